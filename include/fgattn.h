@@ -1,0 +1,152 @@
+/*
+ * fgattn.h -- C ABI of libfgattn.so, the B200 (sm_100a) FG-Attn hot path.
+ *
+ * Drop-in boundary for the reference package `sliceattn`
+ * (/root/reference/pkg/src/sliceattn).  The reference is pure Python/NumPy
+ * and has no FFI of its own; each entry point below is the native body of
+ * one reference operator, and the Python mirror in
+ * paper_2509_16518_b200/ binds them with ctypes exactly as a maintainer of
+ * the reference would.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers owned by the caller (torch); the
+ *     library never allocates or frees caller memory.
+ *   - `stream` is a cudaStream_t passed as void*; every call is
+ *     stream-ordered and asynchronous (no device synchronisation).
+ *   - Q/K/V are bf16 [B, H, N, D] contiguous, D innermost.
+ *   - A "group" is `group_size` (M) consecutive query rows; G = ceil(N/M)
+ *     (core.py:69-76).  Masks are per (b, h, g) rows of N slots.
+ *   - Return 0 on success, a negative FGA_E* code otherwise; the message is
+ *     available from fga_last_error() (thread-local).
+ */
+#ifndef FGATTN_H_
+#define FGATTN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FGA_OK 0
+#define FGA_EINVAL (-1)        /* shape / config error   -> ShapeError / ValueError */
+#define FGA_ERANGE (-2)        /* index out of range     -> IndexError / ValueError */
+#define FGA_ECUDA (-3)         /* CUDA launch / driver   -> RuntimeError            */
+#define FGA_EUNSUPPORTED (-4)  /* D not supported, not sm_100                         */
+
+#define FGA_OUT_BF16 0
+#define FGA_OUT_F32 1
+
+/* Problem shape; mirrors AttnConfig (core.py:32-63).  scale <= 0 means 1/sqrt(D). */
+typedef struct fga_shape {
+  int64_t batch;
+  int64_t heads;
+  int64_t seq_len;
+  int64_t head_dim;
+  int64_t group_size;
+  float scale;
+} fga_shape;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int fga_version(void);
+
+/* Thread-local description of the last failure ("" when none). */
+const char* fga_last_error(void);
+
+/* 1 when `device` is an sm_100 part the kernels were built for, else 0. */
+int fga_device_supported(int device);
+
+/*
+ * Slice-mask compaction (K1b).  Replaces masks.py:75-91 (_lists_from_keep)
+ * followed by sparse.py:165-175 (export_padded).
+ *   keep   : uint8 [rows, n], nonzero = keep key j for that (b,h,g) row.
+ *   scores : optional fp32 [rows, n]; when given, an empty row falls back to
+ *            the first position of its maximum (masks.py:86-87).  When NULL
+ *            an empty row keeps count 0.
+ *   idx    : int32 [rows, idx_stride]; receives the ascending kept positions.
+ *   counts : int32 [rows].
+ *   fill_sentinel : nonzero -> slots [count, n) of each row are set to -1
+ *            (the export_padded layout); zero -> left untouched.
+ */
+int fga_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t n, int32_t* idx,
+                int64_t idx_stride, int32_t* counts, int fill_sentinel, void* stream);
+
+/*
+ * FG-Attn forward (K2 gather producer + K3 tcgen05 consumer).
+ * Replaces sparse.py:111-156 (sparse_attention), whose numerics are the
+ * online softmax of tiled.py:48-77; equals oracle.py:55-82
+ * (masked_dense_attention) within bf16 tolerance.
+ *   idx    : int32, row (b,h,g) at idx + ((b*H+h)*G+g)*idx_group_stride,
+ *            ascending or not, first counts[(b*H+h)*G+g] entries used; all
+ *            entries must lie in [0, N) (checked by the Python mirror).
+ *   counts : int32 [B*H*G], each >= 1.
+ *   o      : [B, H, N, D], bf16 (o_dtype = FGA_OUT_BF16) or fp32 (FGA_OUT_F32).
+ *   lse    : optional fp32 [B, H, N] natural-log softmax normaliser.
+ * Supported: head_dim in {64, 128}; any group_size in [1, N].
+ */
+int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32_t* idx,
+                        int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
+                        fga_shape shape, void* stream);
+
+/*
+ * Dense attention with the same kernel and contiguous key chunks (every group
+ * lists all N keys).  Replaces tiled.py:80-114 (flash_attention) /
+ * oracle.py:29-42 (dense_attention); the dense denominator of the speed-up.
+ */
+int fga_dense_attn_fwd(const void* q, const void* k, const void* v, void* o, int o_dtype, float* lse,
+                       fga_shape shape, void* stream);
+
+/*
+ * Gather-load primitive (K2 in isolation, for bitwise parity).  Replaces
+ * sparse.py:95-108 (gather_rows): out[i, :] = matrix[indices[i], :].
+ *   matrix : bf16 [rows, d], d a multiple of 64, d <= 256.
+ *   indices: int32 [n_idx], each in [0, rows) (duplicates allowed).
+ *   out    : bf16 [n_idx, d].
+ */
+int fga_gather_rows(const void* matrix, int64_t rows, int64_t d, const int32_t* indices, int64_t n_idx,
+                    void* out, void* stream);
+
+/*
+ * Average-query pooled scores (K1a, avg-query builder).  Replaces
+ * masks.py:108-118 (pooled_query_scores):
+ *   scores[b,h,g,j] = exp((k_j . mean_{i in g} q_i) * scale) / D   (fp32),
+ *   rounded to bf16 (RNE, widened) when round_bf16 != 0.
+ *   scores : fp32 [B, H, G, N].
+ */
+int fga_pooled_scores(const void* q, const void* k, fga_shape shape, int round_bf16, float* scores,
+                      void* stream);
+
+/* keep[i] = scores[i] >= tau  (masks.py:132 / masks.py:104). */
+int fga_threshold_keep(const float* scores, int64_t n_elems, float tau, uint8_t* keep, void* stream);
+
+/*
+ * Top-k keep bits per row (masks.py:133-147): the top_k largest scores of
+ * each row, ties broken toward the smaller key index.
+ *   scores : fp32 [rows, n]; keep : uint8 [rows, n].
+ */
+int fga_topk_keep(const float* scores, int64_t rows, int64_t n, int64_t top_k, uint8_t* keep, void* stream);
+
+/*
+ * Cached-threshold statistics (K1a, cached builder) without materialising
+ * the [B,H,N,N] map: pass 1 computes each query row's softmax normaliser,
+ * pass 2 the per-group column maximum of the normalised map.  Replaces
+ * oracle.py:45-52 (attention_map) + masks.py:66-72 (_group_max) as used by
+ * masks.py:94-105 (build_mask_cached).
+ *   gmax   : fp32 [B, H, G, N]; bf16-rounded when round_bf16 != 0.
+ *   row_ws : fp32 workspace of 2*B*H*N floats (row max, row denominator).
+ */
+int fga_cached_group_max(const void* q, const void* k, fga_shape shape, int round_bf16, float* gmax,
+                         float* row_ws, void* stream);
+
+/*
+ * Benchmark masks: every row keeps exactly `count` distinct keys chosen
+ * uniformly at random (the random_mask count rule, sparse.py:216-232, with
+ * a counter-based device RNG -- not NumPy's Philox stream).
+ */
+int fga_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, uint8_t* keep, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FGATTN_H_ */

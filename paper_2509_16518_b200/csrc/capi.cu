@@ -1,0 +1,159 @@
+// C ABI of libfgattn.so (include/fgattn.h): argument validation, error
+// codes, TMA descriptor construction, and dispatch to the kernel launchers.
+#include <cstdio>
+#include <string>
+
+#include "internal.h"
+
+namespace fga {
+
+int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, float* scores, cudaStream_t st);
+int launch_threshold(const float* s, int64_t n, float tau, uint8_t* keep, cudaStream_t st);
+int launch_topk(const float* s, int64_t rows, int64_t n, int64_t k, uint8_t* keep, cudaStream_t st);
+int launch_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, uint8_t* keep, cudaStream_t st);
+int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, float* ws,
+                            cudaStream_t st);
+
+namespace {
+thread_local std::string g_last_error;
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+  static EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+int check_shape(const fga_shape& s) {
+  if (s.batch < 1 || s.heads < 1 || s.seq_len < 1 || s.head_dim < 1 || s.group_size < 1)
+    return fail(FGA_EINVAL, "batch, heads, seq_len, head_dim and group_size must be positive");
+  if (s.group_size > s.seq_len) return fail(FGA_EINVAL, "group_size exceeds seq_len");
+  if (s.seq_len >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "seq_len must be < 2^31");
+  return FGA_OK;
+}
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return FGA_OK;
+  return fail(FGA_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                      uint32_t box_rows) {
+  EncodeTiled enc = encode_fn();
+  if (enc == nullptr) return fail(FGA_ECUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  if ((reinterpret_cast<uintptr_t>(base) & 15u) != 0) return fail(FGA_EINVAL, "tensor base must be 16-byte aligned");
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FGA_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return FGA_OK;
+}
+
+}  // namespace fga
+
+using namespace fga;
+
+extern "C" {
+
+int fga_version(void) { return 100; }
+
+const char* fga_last_error(void) { return g_last_error.c_str(); }
+
+int fga_device_supported(int device) {
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return prop.major == 10 && prop.minor == 0 ? 1 : 0;
+}
+
+int fga_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t n, int32_t* idx, int64_t idx_stride,
+                int32_t* counts, int fill_sentinel, void* stream) {
+  if ((keep == nullptr || idx == nullptr || counts == nullptr) && rows > 0) return fail(FGA_EINVAL, "null pointer");
+  return launch_compact(keep, scores, rows, n, idx, idx_stride, counts, fill_sentinel,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
+                        const int32_t* counts, void* o, int o_dtype, float* lse, fga_shape shape, void* stream) {
+  int rc = check_shape(shape);
+  if (rc != FGA_OK) return rc;
+  if (!q || !k || !v || !idx || !counts || !o) return fail(FGA_EINVAL, "null pointer");
+  if (idx_group_stride < 1) return fail(FGA_EINVAL, "idx_group_stride must be >= 1");
+  if (o_dtype != FGA_OUT_BF16 && o_dtype != FGA_OUT_F32) return fail(FGA_EINVAL, "o_dtype must be FGA_OUT_BF16 or FGA_OUT_F32");
+  return launch_attn(q, k, v, idx, idx_group_stride, counts, o, o_dtype, lse, shape, false,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int fga_dense_attn_fwd(const void* q, const void* k, const void* v, void* o, int o_dtype, float* lse,
+                       fga_shape shape, void* stream) {
+  int rc = check_shape(shape);
+  if (rc != FGA_OK) return rc;
+  if (!q || !k || !v || !o) return fail(FGA_EINVAL, "null pointer");
+  if (o_dtype != FGA_OUT_BF16 && o_dtype != FGA_OUT_F32) return fail(FGA_EINVAL, "o_dtype must be FGA_OUT_BF16 or FGA_OUT_F32");
+  return launch_attn(q, k, v, nullptr, 0, nullptr, o, o_dtype, lse, shape, true, static_cast<cudaStream_t>(stream));
+}
+
+int fga_gather_rows(const void* matrix, int64_t rows, int64_t d, const int32_t* indices, int64_t n_idx, void* out,
+                    void* stream) {
+  if (n_idx > 0 && (!matrix || !indices || !out)) return fail(FGA_EINVAL, "null pointer");
+  return launch_gather(matrix, rows, d, indices, n_idx, out, static_cast<cudaStream_t>(stream));
+}
+
+int fga_pooled_scores(const void* q, const void* k, fga_shape shape, int round_bf16, float* scores, void* stream) {
+  int rc = check_shape(shape);
+  if (rc != FGA_OK) return rc;
+  if (!q || !k || !scores) return fail(FGA_EINVAL, "null pointer");
+  return launch_pooled_scores(q, k, shape, round_bf16, scores, static_cast<cudaStream_t>(stream));
+}
+
+int fga_threshold_keep(const float* scores, int64_t n_elems, float tau, uint8_t* keep, void* stream) {
+  if (n_elems < 0) return fail(FGA_EINVAL, "n_elems must be >= 0");
+  if (n_elems > 0 && (!scores || !keep)) return fail(FGA_EINVAL, "null pointer");
+  return launch_threshold(scores, n_elems, tau, keep, static_cast<cudaStream_t>(stream));
+}
+
+int fga_topk_keep(const float* scores, int64_t rows, int64_t n, int64_t top_k, uint8_t* keep, void* stream) {
+  if (rows < 0 || n < 1) return fail(FGA_EINVAL, "rows must be >= 0 and n >= 1");
+  if (rows > 0 && (!scores || !keep)) return fail(FGA_EINVAL, "null pointer");
+  return launch_topk(scores, rows, n, top_k, keep, static_cast<cudaStream_t>(stream));
+}
+
+int fga_cached_group_max(const void* q, const void* k, fga_shape shape, int round_bf16, float* gmax, float* row_ws,
+                         void* stream) {
+  int rc = check_shape(shape);
+  if (rc != FGA_OK) return rc;
+  if (!q || !k || !gmax || !row_ws) return fail(FGA_EINVAL, "null pointer");
+  return launch_cached_group_max(q, k, shape, round_bf16, gmax, row_ws, static_cast<cudaStream_t>(stream));
+}
+
+int fga_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, uint8_t* keep, void* stream) {
+  if (rows < 0 || n < 1) return fail(FGA_EINVAL, "rows must be >= 0 and n >= 1");
+  if (rows > 0 && !keep) return fail(FGA_EINVAL, "null pointer");
+  return launch_random_keep(rows, n, count, seed, keep, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

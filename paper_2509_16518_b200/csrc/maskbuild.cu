@@ -1,0 +1,375 @@
+// K1a: slice-mask construction on the GPU (the step before compaction).
+//
+//   fga_pooled_scores    masks.py:108-118  exp((k_j . mean_g q) * scale) / D  [bf16-rounded]
+//   fga_threshold_keep   masks.py:104 / :132  keep = s >= tau
+//   fga_topk_keep        masks.py:133-147  top_k largest, ties -> smaller index
+//   fga_cached_group_max oracle.py:45-52 + masks.py:66-72  max over a group's rows of
+//                        the normalised attention map, without materialising it
+//   fga_random_keep      sparse.py:216-232 count rule (device RNG, benchmark masks)
+// (paths relative to /root/reference/pkg/src/sliceattn/)
+//
+// Scores are fp32 CUDA-core dot products with a sequential-in-d FMA chain so
+// results sit within a few ulp of NumPy; keep bits are compared exactly in
+// tests (report any flip with |s - tau| within ulps).
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include "internal.h"
+
+namespace fga {
+namespace {
+
+__device__ __forceinline__ float bf16_rne(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ float ld_bf16(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+// ------------------------------------------------------------ pooled scores
+// qbar[bhg, d] = (sum_{i in g} q[bh, i, d]) / rows   (sequential fp32 sum, as np.mean over axis 2)
+__global__ void pooled_mean_kernel(const __nv_bfloat16* __restrict__ q, float* __restrict__ qbar, int N, int D,
+                                   int M, int G) {
+  const int64_t bhg = blockIdx.x;
+  const int g = static_cast<int>(bhg % G);
+  const int64_t bh = bhg / G;
+  const int lo = g * M, hi = min(lo + M, N);
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.f;
+    for (int i = lo; i < hi; ++i) acc = __fadd_rn(acc, ld_bf16(q + (bh * N + i) * D + d));
+    qbar[bhg * D + d] = __fdiv_rn(acc, static_cast<float>(hi - lo));
+  }
+}
+
+// 64x64 fp32 tile of A[rows, D] . B[cols, D]^T, 256 threads, 4x4 per thread.
+// A and B rows are fetched through loader functors (bf16 or fp32 sources).
+constexpr int TILE = 64, DK = 32;
+
+template <typename LA, typename LB>
+__device__ __forceinline__ void dot_tile(LA la, LB lb, int D, float (&acc)[4][4]) {
+  __shared__ float As[TILE][DK + 1];
+  __shared__ float Bs[TILE][DK + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.f;
+  for (int d0 = 0; d0 < D; d0 += DK) {
+    for (int e = tid; e < TILE * DK; e += 256) {
+      const int rr = e / DK, dd = e % DK;
+      As[rr][dd] = la(rr, d0 + dd);
+      Bs[rr][dd] = lb(rr, d0 + dd);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int dd = 0; dd < DK; ++dd) {
+      float a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = As[ty + 16 * r][dd];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = Bs[tx + 16 * c][dd];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = __fmaf_rn(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+}
+
+// scores[bh, g, j] for a 64(g) x 64(j) tile.  grid: (key tiles, group tiles, B*H)
+__global__ void __launch_bounds__(256) pooled_scores_kernel(const float* __restrict__ qbar,
+                                                            const __nv_bfloat16* __restrict__ k,
+                                                            float* __restrict__ scores, int N, int D, int G,
+                                                            float scale, int round) {
+  const int64_t bh = blockIdx.z;
+  const int g0 = blockIdx.y * TILE, j0 = blockIdx.x * TILE;
+  float acc[4][4];
+  dot_tile(
+      [&](int r, int d) { const int g = g0 + r; return g < G ? qbar[(bh * G + g) * D + d] : 0.f; },
+      [&](int r, int d) { const int j = j0 + r; return j < N ? ld_bf16(k + (bh * N + j) * D + d) : 0.f; }, D, acc);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const float inv_d = static_cast<float>(D);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int g = g0 + ty + 16 * r;
+    if (g >= G) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + tx + 16 * c;
+      if (j >= N) continue;
+      float s = __fdiv_rn(expf(__fmul_rn(acc[r][c], scale)), inv_d);
+      if (round) s = bf16_rne(s);
+      scores[(bh * G + g) * N + j] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------ threshold
+__global__ void threshold_kernel(const float* __restrict__ s, int64_t n, float tau, uint8_t* __restrict__ keep) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    keep[i] = s[i] >= tau ? 1 : 0;
+}
+
+// ------------------------------------------------------------ top-k / random
+__device__ __forceinline__ uint32_t float_key(float x) {  // order-preserving float -> uint32
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ uint32_t mix32(uint64_t x) {  // splitmix64 finaliser
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return static_cast<uint32_t>(x >> 32);
+}
+
+struct FloatKeys {
+  const float* s;
+  __device__ uint32_t operator()(int64_t row, int64_t n, int64_t i) const { return float_key(s[row * n + i]); }
+};
+struct HashKeys {
+  uint64_t seed;
+  __device__ uint32_t operator()(int64_t row, int64_t n, int64_t i) const {
+    return mix32(seed * 0xD1B54A32D192ED03ull ^ (static_cast<uint64_t>(row) * n + i));
+  }
+};
+
+constexpr int TK = 512;
+
+// Keep the k largest keys of each row; among keys equal to the k-th largest,
+// keep the ones with the smallest indices.  4 radix-select passes + 1 ordered pass.
+template <typename Keys>
+__global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t k, uint8_t* __restrict__ keep) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t s_prefix;
+  __shared__ int64_t s_rem;
+  __shared__ int s_warp[TK / 32];
+  __shared__ int s_tot;
+  const int64_t row = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t prefix = 0, mask = 0;
+  int64_t rem = k;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int b = tid; b < 256; b += TK) hist[b] = 0;
+    __syncthreads();
+    for (int64_t i = tid; i < n; i += TK) {
+      const uint32_t key = keys(row, n, i);
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int64_t cum = 0;
+      int b = 255;
+      for (; b > 0; --b) {
+        if (cum + hist[b] >= rem) break;
+        cum += hist[b];
+      }
+      s_prefix = prefix | (static_cast<uint32_t>(b) << shift);
+      s_rem = rem - cum;
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    rem = s_rem;
+    mask |= 255u << shift;
+    __syncthreads();
+  }
+  // prefix is the k-th largest key; keep all larger keys and the first `rem` equal ones.
+  int64_t taken = 0;
+  for (int64_t base = 0; base < n; base += TK) {
+    const int64_t i = base + tid;
+    uint32_t key = 0;
+    if (i < n) key = keys(row, n, i);
+    const bool gt = i < n && key > prefix;
+    const bool eq = i < n && key == prefix;
+    const unsigned bal = __ballot_sync(0xffffffffu, eq);
+    const int in_warp = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) s_warp[warp] = __popc(bal);
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int w = 0; w < TK / 32; ++w) { const int t = s_warp[w]; s_warp[w] = run; run += t; }
+      s_tot = run;
+    }
+    __syncthreads();
+    const int64_t rank = taken + s_warp[warp] + in_warp;
+    if (i < n) keep[row * n + i] = (gt || (eq && rank < rem)) ? 1 : 0;
+    taken += s_tot;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ cached builder
+// Pass 1: per query row, max_j s_ij (mode 0) or sum_j exp(s_ij - max) in fp64 (mode 1).
+// grid: (query tiles, B*H); each block walks every key tile.
+template <int MODE>
+__global__ void __launch_bounds__(256) row_stats_kernel(const __nv_bfloat16* __restrict__ q,
+                                                        const __nv_bfloat16* __restrict__ k, int N, int D,
+                                                        float scale, float* __restrict__ row_max,
+                                                        double* __restrict__ row_den) {
+  const int64_t bh = blockIdx.y;
+  const int i0 = blockIdx.x * TILE;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  __shared__ float red_f[TILE][17];
+  __shared__ double red_d[TILE][17];
+  float mx[4];
+  double den[4];
+  float mrow[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    mx[r] = -INFINITY;
+    den[r] = 0.0;
+    const int i = i0 + ty + 16 * r;
+    mrow[r] = (MODE == 1 && i < N) ? row_max[bh * N + i] : 0.f;
+  }
+  for (int j0 = 0; j0 < N; j0 += TILE) {
+    float acc[4][4];
+    dot_tile([&](int r, int d) { const int i = i0 + r; return i < N ? ld_bf16(q + (bh * N + i) * D + d) : 0.f; },
+             [&](int r, int d) { const int j = j0 + r; return j < N ? ld_bf16(k + (bh * N + j) * D + d) : 0.f; }, D,
+             acc);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int j = j0 + tx + 16 * c;
+        if (j >= N) continue;
+        const float s = __fmul_rn(acc[r][c], scale);
+        if (MODE == 0) mx[r] = fmaxf(mx[r], s);
+        else den[r] += static_cast<double>(expf(__fsub_rn(s, mrow[r])));
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if (MODE == 0) red_f[ty + 16 * r][tx] = mx[r];
+    else red_d[ty + 16 * r][tx] = den[r];
+  }
+  __syncthreads();
+  if (threadIdx.x < TILE) {
+    const int rr = threadIdx.x, i = i0 + rr;
+    if (i < N) {
+      if (MODE == 0) {
+        float m = -INFINITY;
+        for (int t = 0; t < 16; ++t) m = fmaxf(m, red_f[rr][t]);
+        row_max[bh * N + i] = m;
+      } else {
+        double s = 0.0;
+        for (int t = 0; t < 16; ++t) s += red_d[rr][t];
+        row_den[bh * N + i] = s;
+      }
+    }
+  }
+}
+
+// Pass 2: gmax[bh, g, j] = max_{i in g} float(exp(s_ij - max_i) / den_i).  grid: (key tiles, G, B*H)
+__global__ void __launch_bounds__(256) group_max_kernel(const __nv_bfloat16* __restrict__ q,
+                                                        const __nv_bfloat16* __restrict__ k, int N, int D, int M,
+                                                        int G, float scale, const float* __restrict__ row_max,
+                                                        const double* __restrict__ row_den, int round,
+                                                        float* __restrict__ gmax) {
+  const int64_t bh = blockIdx.z;
+  const int g = blockIdx.y, j0 = blockIdx.x * TILE;
+  const int lo = g * M, hi = min(lo + M, N);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  __shared__ float red[16][TILE];
+  float best[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  for (int i0 = lo; i0 < hi; i0 += TILE) {
+    float acc[4][4];
+    dot_tile([&](int r, int d) { const int i = i0 + r; return i < hi ? ld_bf16(q + (bh * N + i) * D + d) : 0.f; },
+             [&](int r, int d) { const int j = j0 + r; return j < N ? ld_bf16(k + (bh * N + j) * D + d) : 0.f; }, D,
+             acc);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = i0 + ty + 16 * r;
+      if (i >= hi) continue;
+      const float m = row_max[bh * N + i];
+      const double den = row_den[bh * N + i];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float s = __fmul_rn(acc[r][c], scale);
+        const float a = static_cast<float>(static_cast<double>(expf(__fsub_rn(s, m))) / den);
+        best[c] = fmaxf(best[c], a);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) red[ty][tx + 16 * c] = best[c];
+  __syncthreads();
+  if (threadIdx.x < TILE) {
+    const int j = j0 + threadIdx.x;
+    if (j < N) {
+      float m = -INFINITY;
+      for (int t = 0; t < 16; ++t) m = fmaxf(m, red[t][threadIdx.x]);
+      if (round) m = bf16_rne(m);
+      gmax[(bh * G + g) * N + j] = m;
+    }
+  }
+}
+
+int grid1d(int64_t n) { const int64_t b = (n + 255) / 256; return static_cast<int>(b < 148 * 32 ? b : 148 * 32); }
+
+}  // namespace
+
+int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, float* scores,
+                         cudaStream_t st) {
+  const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
+  const int64_t G = (N + M - 1) / M;
+  if (D % DK != 0) return fail(FGA_EUNSUPPORTED, "pooled_scores: head_dim must be a multiple of 32");
+  float* qbar = nullptr;
+  if (cudaMallocAsync(&qbar, sizeof(float) * B * H * G * D, st) != cudaSuccess) return check_launch("cudaMallocAsync");
+  pooled_mean_kernel<<<static_cast<unsigned>(B * H * G), 128, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N), static_cast<int>(D), static_cast<int>(M),
+      static_cast<int>(G));
+  const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
+  dim3 grid(static_cast<unsigned>((N + TILE - 1) / TILE), static_cast<unsigned>((G + TILE - 1) / TILE),
+            static_cast<unsigned>(B * H));
+  pooled_scores_kernel<<<grid, 256, 0, st>>>(qbar, static_cast<const __nv_bfloat16*>(k), scores,
+                                             static_cast<int>(N), static_cast<int>(D), static_cast<int>(G), scale,
+                                             round);
+  int rc = check_launch("pooled_scores_kernel");
+  cudaFreeAsync(qbar, st);
+  return rc;
+}
+
+int launch_threshold(const float* s, int64_t n, float tau, uint8_t* keep, cudaStream_t st) {
+  if (n == 0) return FGA_OK;
+  threshold_kernel<<<grid1d(n), 256, 0, st>>>(s, n, tau, keep);
+  return check_launch("threshold_kernel");
+}
+
+int launch_topk(const float* s, int64_t rows, int64_t n, int64_t k, uint8_t* keep, cudaStream_t st) {
+  if (k < 1 || k > n) return fail(FGA_EINVAL, "top_k must be in [1, n]");
+  if (rows == 0) return FGA_OK;
+  topk_kernel<<<static_cast<unsigned>(rows), TK, 0, st>>>(FloatKeys{s}, n, k, keep);
+  return check_launch("topk_kernel");
+}
+
+int launch_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, uint8_t* keep, cudaStream_t st) {
+  if (count < 1 || count > n) return fail(FGA_EINVAL, "random_keep: count must be in [1, n]");
+  if (rows == 0) return FGA_OK;
+  topk_kernel<<<static_cast<unsigned>(rows), TK, 0, st>>>(HashKeys{seed}, n, count, keep);
+  return check_launch("topk_kernel(random)");
+}
+
+int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, float* ws,
+                            cudaStream_t st) {
+  const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
+  const int64_t G = (N + M - 1) / M;
+  if (D % DK != 0) return fail(FGA_EUNSUPPORTED, "cached_group_max: head_dim must be a multiple of 32");
+  const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
+  // workspace: row max (fp32) in the first B*H*N floats; the fp64 denominators need 8-byte slots,
+  // so they live in a temporary buffer.
+  float* row_max = ws;
+  double* row_den = nullptr;
+  if (cudaMallocAsync(&row_den, sizeof(double) * B * H * N, st) != cudaSuccess) return check_launch("cudaMallocAsync");
+  const auto* qb = static_cast<const __nv_bfloat16*>(q);
+  const auto* kb = static_cast<const __nv_bfloat16*>(k);
+  dim3 g1(static_cast<unsigned>((N + TILE - 1) / TILE), static_cast<unsigned>(B * H));
+  row_stats_kernel<0><<<g1, 256, 0, st>>>(qb, kb, static_cast<int>(N), static_cast<int>(D), scale, row_max, row_den);
+  row_stats_kernel<1><<<g1, 256, 0, st>>>(qb, kb, static_cast<int>(N), static_cast<int>(D), scale, row_max, row_den);
+  dim3 g2(static_cast<unsigned>((N + TILE - 1) / TILE), static_cast<unsigned>(G), static_cast<unsigned>(B * H));
+  group_max_kernel<<<g2, 256, 0, st>>>(qb, kb, static_cast<int>(N), static_cast<int>(D), static_cast<int>(M),
+                                       static_cast<int>(G), scale, row_max, row_den, round, gmax);
+  int rc = check_launch("cached_group_max");
+  cudaFreeAsync(row_den, st);
+  return rc;
+}
+
+}  // namespace fga

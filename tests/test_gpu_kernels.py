@@ -1,0 +1,297 @@
+"""Kernel-level parity of libfgattn.so against the CPU oracle (GPU only).
+
+Every call goes through the C ABI (ctypes) on torch-owned device memory.
+Tolerances: indices/keep bits/gathered rows are bit-exact; attention outputs
+<= 2e-2 max-abs vs the reference fp32 result (BASELINE.json north_star).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN_CASES, cuda_ok
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not cuda_ok():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2509_16518_b200 import _lib  # noqa: E402
+
+ATOL = 2e-2
+
+
+def ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def to_bf16_dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda().to(torch.bfloat16)
+
+
+def padded_dev(lists, b, h, n, m):
+    g = oracle.num_groups(n, m)
+    pad = oracle.lists_to_padded(lists, b, h, g, n)
+    counts = (pad >= 0).sum(-1).astype(np.int32)
+    return torch.from_numpy(pad).cuda(), torch.from_numpy(counts).cuda()
+
+
+def run_sparse(q, k, v, idx, counts, b, h, n, d, m, scale=None, out_f32=True, lse=False):
+    o = torch.empty((b, h, n, d), device="cuda", dtype=torch.float32 if out_f32 else torch.bfloat16)
+    l = torch.empty((b, h, n), device="cuda", dtype=torch.float32) if lse else None
+    _lib.call("fga_sparse_attn_fwd", ptr(q), ptr(k), ptr(v), ptr(idx), idx.shape[-1], ptr(counts), ptr(o),
+              _lib.FGA_OUT_F32 if out_f32 else _lib.FGA_OUT_BF16, ptr(l), _lib.shape(b, h, n, d, m, scale), stream())
+    torch.cuda.synchronize()
+    return o, l
+
+
+# ------------------------------------------------------------------ K2 gather
+
+@pytest.mark.parametrize("d", [64, 128, 192, 256])
+@pytest.mark.parametrize("n_idx", [1, 5, 128, 300])
+def test_gather_rows_bitwise(d, n_idx):
+    g = torch.Generator().manual_seed(d + n_idx)
+    mat = torch.randn(777, d, generator=g).to(torch.bfloat16).cuda()
+    idx = torch.randint(0, 777, (n_idx,), generator=g, dtype=torch.int32)
+    idx[: min(3, n_idx)] = 776  # duplicates + last row
+    idx = idx.cuda()
+    out = torch.empty(n_idx, d, dtype=torch.bfloat16, device="cuda")
+    _lib.call("fga_gather_rows", ptr(mat), 777, d, ptr(idx), n_idx, ptr(out), stream())
+    torch.cuda.synchronize()
+    ref = mat[idx.long()]
+    assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+
+
+# ------------------------------------------------------------------ K1b compaction
+
+@pytest.mark.parametrize("n", [33, 1000, 4096, 32760])
+@pytest.mark.parametrize("fill", [0, 1])
+def test_compact_bit_exact(n, fill):
+    rng = np.random.default_rng(n)
+    rows = 37
+    keep = (rng.random((rows, n)) < rng.random((rows, 1))).astype(np.uint8)
+    keep[3] = 0   # empty row -> argmax fallback
+    keep[4] = 1   # full row
+    keep[5] = 0
+    keep[5, n - 1] = 7   # nonzero != 1 counts as kept
+    scores = rng.standard_normal((rows, n)).astype(np.float32)
+    scores[3, 11] = scores[3].max() + 1
+    scores[3, 17] = scores[3, 11]   # tie -> first max (11)
+    ref = oracle.lists_to_padded(oracle.keep_to_lists(keep, scores), 1, 1, rows, n)[0, 0]
+    idx = torch.full((rows, n), 12345, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(rows, dtype=torch.int32, device="cuda")
+    kd = torch.from_numpy(keep).cuda()
+    sd = torch.from_numpy(scores).cuda()
+    _lib.call("fga_compact", ptr(kd), ptr(sd), rows, n, ptr(idx), n, ptr(cnt), fill, stream())
+    torch.cuda.synchronize()
+    got = idx.cpu().numpy()
+    c = cnt.cpu().numpy()
+    assert np.array_equal(c, (ref >= 0).sum(-1))
+    if fill:
+        assert np.array_equal(got, ref)
+    else:
+        for r in range(rows):
+            assert np.array_equal(got[r, : c[r]], ref[r, : c[r]])
+            assert (got[r, c[r]:] == 12345).all()
+
+
+def test_compact_unaligned_rows_without_scores():
+    # row starts at odd byte offsets (n = 13) and no fallback: empty rows keep count 0
+    rng = np.random.default_rng(1)
+    keep = (rng.random((50, 13)) < 0.3).astype(np.uint8)
+    keep[7] = 0
+    idx = torch.zeros((50, 16), dtype=torch.int32, device="cuda")
+    cnt = torch.empty(50, dtype=torch.int32, device="cuda")
+    kd = torch.from_numpy(keep).cuda()
+    _lib.call("fga_compact", ptr(kd), None, 50, 13, ptr(idx), 16, ptr(cnt), 1, stream())
+    torch.cuda.synchronize()
+    c = cnt.cpu().numpy()
+    got = idx.cpu().numpy()
+    for r in range(50):
+        pos = np.flatnonzero(keep[r])
+        assert c[r] == pos.size
+        assert np.array_equal(got[r, : c[r]], pos)
+        assert (got[r, c[r]:13] == -1).all()
+
+
+# ------------------------------------------------------------------ K2+K3 attention
+
+ATTN_CASES = [c for c in GOLDEN_CASES if c != "avgq_topk_ties"]
+
+
+@pytest.mark.parametrize("name", ATTN_CASES)
+@pytest.mark.parametrize("out_f32", [True, False])
+def test_sparse_attention_matches_reference_golden(golden, name, out_f32):
+    g = golden(name)
+    b, h, n, d = g.shape
+    m = g.group_size
+    q, k, v = (to_bf16_dev(oracle.bf16_round(t)) for t in (g.q, g.k, g.v))
+    idx = torch.from_numpy(g["padded"].astype(np.int32)).cuda()
+    cnt = torch.from_numpy(g["counts"].astype(np.int32)).cuda()
+    o, lse = run_sparse(q, k, v, idx, cnt, b, h, n, d, m, g.cfg["scale"], out_f32, lse=True)
+    ref = g["sparse_out"]
+    err = np.abs(o.float().cpu().numpy() - ref).max()
+    assert err <= ATOL, f"{name}: max-abs {err}"
+    assert torch.isfinite(lse).all()
+
+
+def test_sparse_attention_c1_error_is_small(golden):
+    # tighter than the contract: fp32 out at c1 should sit near the bf16-P error (~1e-3)
+    g = golden("c1_random30")
+    b, h, n, d = g.shape
+    q, k, v = (to_bf16_dev(oracle.bf16_round(t)) for t in (g.q, g.k, g.v))
+    idx = torch.from_numpy(g["padded"].astype(np.int32)).cuda()
+    cnt = torch.from_numpy(g["counts"].astype(np.int32)).cuda()
+    o, _ = run_sparse(q, k, v, idx, cnt, b, h, n, d, 128, None, True)
+    err = np.abs(o.cpu().numpy() - g["sparse_out"]).max()
+    assert err <= 5e-3, err
+
+
+def test_single_key_groups_copy_value_row():
+    # a single listed key -> every output row equals v_j
+    b, h, n, d, m = 1, 2, 512, 128, 128
+    rng = np.random.default_rng(3)
+    q, k, v = (oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32)) for _ in range(3))
+    g = oracle.num_groups(n, m)
+    lists = [np.array([int(rng.integers(n))]) for _ in range(b * h * g)]
+    idx, cnt = padded_dev(lists, b, h, n, m)
+    o, _ = run_sparse(to_bf16_dev(q), to_bf16_dev(k), to_bf16_dev(v), idx, cnt, b, h, n, d, m)
+    o = o.cpu().numpy()
+    for r, lst in enumerate(lists):
+        bb, hh, gg = r // (h * g), (r // g) % h, r % g
+        assert np.array_equal(o[bb, hh, gg * m:(gg + 1) * m], np.broadcast_to(v[bb, hh, lst[0]], (m, d)))
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_unsorted_duplicate_free_lists_and_stride(d):
+    # kernel consumes lists in the given order; result is order-independent
+    b, h, n, m = 1, 1, 700, 128
+    rng = np.random.default_rng(d)
+    q, k, v = (oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32)) for _ in range(3))
+    g = oracle.num_groups(n, m)
+    lists = [np.sort(rng.choice(n, size=int(rng.integers(1, n)), replace=False)) for _ in range(g)]
+    ref = oracle.masked_attention(q, k, v, lists, m)
+    stride = n + 9
+    pad = np.full((g, stride), -1, np.int32)
+    counts = np.zeros(g, np.int32)
+    for i, lst in enumerate(lists):
+        perm = rng.permutation(lst)
+        pad[i, : len(lst)] = perm
+        counts[i] = len(lst)
+    o, _ = run_sparse(to_bf16_dev(q), to_bf16_dev(k), to_bf16_dev(v), torch.from_numpy(pad).cuda(),
+                      torch.from_numpy(counts).cuda(), b, h, n, d, m)
+    assert np.abs(o.cpu().numpy() - ref).max() <= ATOL
+
+
+@pytest.mark.parametrize("m", [16, 64, 200, 256])
+def test_group_sizes(m):
+    b, h, n, d = 1, 2, 600, 64
+    rng = np.random.default_rng(m)
+    q, k, v = (oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32)) for _ in range(3))
+    lists = oracle.random_lists(b, h, n, m, 0.3, seed=m)
+    ref = oracle.masked_attention(q, k, v, lists, m)
+    idx, cnt = padded_dev(lists, b, h, n, m)
+    o, _ = run_sparse(to_bf16_dev(q), to_bf16_dev(k), to_bf16_dev(v), idx, cnt, b, h, n, d, m)
+    assert np.abs(o.cpu().numpy() - ref).max() <= ATOL
+
+
+@pytest.mark.parametrize("d,n", [(64, 1000), (128, 384)])
+def test_dense_kernel_matches_dense_oracle(d, n):
+    b, h = 1, 2
+    rng = np.random.default_rng(n)
+    q, k, v = (oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32)) for _ in range(3))
+    ref = oracle.dense_attention(q, k, v)
+    o = torch.empty((b, h, n, d), device="cuda", dtype=torch.float32)
+    qd, kd, vd = to_bf16_dev(q), to_bf16_dev(k), to_bf16_dev(v)  # keep alive across the launch
+    _lib.call("fga_dense_attn_fwd", ptr(qd), ptr(kd), ptr(vd), ptr(o),
+              _lib.FGA_OUT_F32, None, _lib.shape(b, h, n, d, 128), stream())
+    torch.cuda.synchronize()
+    assert np.abs(o.cpu().numpy() - ref).max() <= ATOL
+
+
+def test_lse_matches_oracle():
+    b, h, n, d, m = 1, 1, 256, 64, 128
+    rng = np.random.default_rng(5)
+    q, k, v = (oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32)) for _ in range(3))
+    lists = oracle.random_lists(b, h, n, m, 0.5, seed=1)
+    idx, cnt = padded_dev(lists, b, h, n, m)
+    _, lse = run_sparse(to_bf16_dev(q), to_bf16_dev(k), to_bf16_dev(v), idx, cnt, b, h, n, d, m, lse=True)
+    lse = lse.cpu().numpy()
+    for gi, (lo, hi) in enumerate(oracle.group_ranges(n, m)):
+        s = q[0, 0, lo:hi] @ k[0, 0, lists[gi]].T / np.sqrt(d)
+        ref = np.log(np.exp(s - s.max(1, keepdims=True)).sum(1)) + s.max(1)
+        assert np.abs(lse[0, 0, lo:hi] - ref).max() < 1e-3
+
+
+# ------------------------------------------------------------------ K1a builders
+
+def test_pooled_scores_and_threshold_keep(golden):
+    g = golden("avgq_thr")
+    b, h, n, d = g.shape
+    m = g.group_size
+    q, k = (to_bf16_dev(oracle.bf16_round(t)) for t in (g.q, g.k))
+    gcount = oracle.num_groups(n, m)
+    s = torch.empty((b, h, gcount, n), device="cuda", dtype=torch.float32)
+    _lib.call("fga_pooled_scores", ptr(q), ptr(k), _lib.shape(b, h, n, d, m), 1, ptr(s), stream())
+    keep = torch.empty((b, h, gcount, n), device="cuda", dtype=torch.uint8)
+    tau = float(g["tau"])
+    _lib.call("fga_threshold_keep", ptr(s), s.numel(), tau, ptr(keep), stream())
+    torch.cuda.synchronize()
+    ref = g["scores"]
+    got = s.cpu().numpy()
+    # scores are bf16-rounded fp32 dot products: equal except at rare rounding boundaries
+    mism = got != ref
+    assert mism.mean() < 1e-3
+    assert np.abs(got - ref)[mism].max(initial=0) <= np.abs(ref).max() * 2 ** -7
+    flips = (keep.cpu().numpy() != (ref >= tau))
+    assert (flips <= mism).all()   # a keep bit can only flip where the score itself differs
+
+
+def test_topk_keep_matches_reference(golden):
+    for name in ("avgq_thr", "avgq_topk_ties"):
+        g = golden(name)
+        scores = g["scores"]
+        b, h, gc, n = scores.shape
+        top_k = int(g["top_k"])
+        sd = torch.from_numpy(scores).cuda()
+        keep = torch.empty(scores.shape, dtype=torch.uint8, device="cuda")
+        _lib.call("fga_topk_keep", ptr(sd), b * h * gc, n, top_k, ptr(keep), stream())
+        torch.cuda.synchronize()
+        lists = oracle.keep_to_lists(keep.cpu().numpy(), scores)
+        ref = g.lists("topk_padded" if name == "avgq_thr" else "padded")
+        assert all(np.array_equal(a, r) for a, r in zip(lists, ref)), name
+
+
+def test_cached_group_max(golden):
+    g = golden("cached_thr")
+    b, h, n, d = g.shape
+    m = g.group_size
+    q, k = (to_bf16_dev(oracle.bf16_round(t)) for t in (g.q, g.k))
+    gc = oracle.num_groups(n, m)
+    gmax = torch.empty((b, h, gc, n), device="cuda", dtype=torch.float32)
+    ws = torch.empty(2 * b * h * n, device="cuda", dtype=torch.float32)
+    _lib.call("fga_cached_group_max", ptr(q), ptr(k), _lib.shape(b, h, n, d, m), 1, ptr(gmax), ptr(ws), stream())
+    torch.cuda.synchronize()
+    got = gmax.cpu().numpy()
+    ref = g["gmax"]
+    mism = got != ref
+    assert mism.mean() < 1e-3
+    tau = float(g["tau"])
+    flips = (got >= tau) != (ref >= tau)
+    assert (flips <= mism).all()
+
+
+def test_random_keep_exact_counts():
+    rows, n, count = 64, 32760, 14742
+    keep = torch.empty((rows, n), dtype=torch.uint8, device="cuda")
+    _lib.call("fga_random_keep", rows, n, count, 1234, ptr(keep), stream())
+    torch.cuda.synchronize()
+    c = keep.sum(-1, dtype=torch.int64).cpu()
+    assert (c == count).all()
+    # rows differ from each other
+    assert not torch.equal(keep[0], keep[1])
