@@ -1,0 +1,81 @@
+// Shared definitions of the FG-Attn attention kernels (tile decode, params,
+// epilogue stores).
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "ptx.cuh"
+
+namespace fga {
+
+constexpr int BM = 128;         // query rows per tile (UMMA M)
+constexpr int BN = 128;         // keys per chunk
+constexpr int HALF = BM * 128;  // one SW128 block: 128 rows x 64 bf16 = 16 KB
+
+struct AttnParams {
+  const void* k;  // raw bf16 [B*H*N, D] (cp.async gather source)
+  const void* v;
+  const int32_t* idx;
+  int64_t idx_group_stride;
+  const int32_t* counts;
+  void* out;
+  float* lse;
+  int64_t n_tiles;
+  int heads, seq_len, group_size, groups, tiles_per_group;
+  float scale_log2;
+  int dense;
+};
+
+// One work tile: <=128 query rows of group (b,h,g) and that group's key list.
+struct Tile {
+  int64_t bhg;
+  int q0;       // first query row within the head
+  int rows;     // valid query rows in this tile
+  int row0;     // first row of head (b,h) in the [B*H*N, D] view
+  int count;    // keys in the list
+  int nchunks;  // ceil(count / BN)
+  const int32_t* list;
+};
+
+__device__ __forceinline__ Tile decode_tile(const AttnParams& p, int64_t tile) {
+  Tile t;
+  const int sub = static_cast<int>(tile % p.tiles_per_group);
+  t.bhg = tile / p.tiles_per_group;
+  const int g = static_cast<int>(t.bhg % p.groups);
+  const int64_t bh = t.bhg / p.groups;
+  t.q0 = g * p.group_size + sub * BM;
+  const int q_end = min(g * p.group_size + p.group_size, p.seq_len);
+  t.rows = min(BM, q_end - t.q0);
+  t.row0 = static_cast<int>(bh * p.seq_len);
+  t.count = p.dense ? p.seq_len : __ldg(p.counts + t.bhg);
+  t.nchunks = (t.count + BN - 1) / BN;
+  t.list = p.dense ? nullptr : p.idx + t.bhg * p.idx_group_stride;
+  return t;
+}
+
+// Store 32 fp32 accumulator columns (scaled) of one output row.
+template <bool OUT_F32>
+__device__ __forceinline__ void store_row32(void* out, int64_t off, const uint32_t (&o)[32], float scale) {
+  if constexpr (OUT_F32) {
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(out) + off);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      dst[i] = make_float4(__uint_as_float(o[4 * i]) * scale, __uint_as_float(o[4 * i + 1]) * scale,
+                           __uint_as_float(o[4 * i + 2]) * scale, __uint_as_float(o[4 * i + 3]) * scale);
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + off);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * scale, __uint_as_float(o[8 * i + 1]) * scale),
+                          pack_bf16(__uint_as_float(o[8 * i + 2]) * scale, __uint_as_float(o[8 * i + 3]) * scale),
+                          pack_bf16(__uint_as_float(o[8 * i + 4]) * scale, __uint_as_float(o[8 * i + 5]) * scale),
+                          pack_bf16(__uint_as_float(o[8 * i + 6]) * scale, __uint_as_float(o[8 * i + 7]) * scale));
+  }
+}
+
+int launch_attn_ws(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
+int launch_attn_sync(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
+
+}  // namespace fga

@@ -9,12 +9,18 @@
 // full-width with a repeated valid key and its extra score columns are set to
 // -inf, so they contribute exactly zero (sparse.py:145-146 processes it short).
 //
-// Version 1 ("sync"): 4 warps, thread t owns query row t (TMEM lane t).  The
-// K/V stages are double-buffered (the gather of chunk j+2 overlaps chunk j+1);
-// QK^T, softmax and PV are serialised inside the CTA.
+// This file holds the host launcher (tensor maps, parameters, dispatch) and
+// version 1 ("sync"), kept as a debugging reference selectable with
+// FGA_ATTN_KERNEL=sync: 4 warps, thread t owns query row t (TMEM lane t), K/V
+// stages double-buffered, QK^T / softmax / PV serialised inside the CTA.
+// The default path is the warp-specialised kernel in attn_ws.cu.
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "attn_common.cuh"
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -23,10 +29,7 @@ namespace fga {
 
 namespace {
 
-constexpr int BM = 128;        // query rows per tile (UMMA M)
-constexpr int BN = 128;        // keys per chunk
-constexpr int NST = 2;         // K/V pipeline stages
-constexpr int HALF = BM * 128;  // one SW128 block: 128 rows x 64 bf16 = 16 KB
+constexpr int NST = 2;          // K/V pipeline stages
 constexpr int TMEM_COLS = 256;  // S: 128 fp32 columns, O: D columns
 
 template <int D>
@@ -39,17 +42,6 @@ struct Smem {
   static constexpr int OFF_BAR = OFF_P + 2 * HALF;
   static constexpr int BYTES = OFF_BAR + 128;
   static constexpr int ALLOC = BYTES + 1024;  // 1024 B alignment slack (SW128 atoms)
-};
-
-struct AttnParams {
-  const int32_t* idx;
-  int64_t idx_group_stride;
-  const int32_t* counts;
-  void* out;
-  float* lse;
-  int heads, seq_len, group_size, groups, tiles_per_group;
-  float scale_log2;
-  int dense;
 };
 
 // K2: one warp gathers chunk j (128 keys) of K and V into one stage.  Lane l
@@ -98,19 +90,9 @@ __global__ void __launch_bounds__(128, 1)
   const int warp = tid >> 5;
   const int lane = tid & 31;
 
-  // ---- tile decode: blockIdx -> (b*H+h, g, sub-tile of 128 rows)
-  const int64_t tile = blockIdx.x;
-  const int sub = static_cast<int>(tile % p.tiles_per_group);
-  const int64_t bhg = tile / p.tiles_per_group;
-  const int g = static_cast<int>(bhg % p.groups);
-  const int64_t bh = bhg / p.groups;
-  const int q0 = g * p.group_size + sub * BM;
-  const int q_end = min(g * p.group_size + p.group_size, p.seq_len);
-  const int rows = min(BM, q_end - q0);
-  const int row0 = static_cast<int>(bh * p.seq_len);  // first row of this head in the [B*H*N, D] view
-  const int count = p.dense ? p.seq_len : __ldg(p.counts + bhg);
-  const int32_t* list = p.dense ? nullptr : p.idx + bhg * p.idx_group_stride;
-  const int nchunks = (count + BN - 1) / BN;
+  const Tile tl = decode_tile(p, blockIdx.x);
+  const int q0 = tl.q0, rows = tl.rows, row0 = tl.row0, count = tl.count, nchunks = tl.nchunks;
+  const int32_t* list = tl.list;
 
   if (tid == 0) {
     prefetch_tmap(&tmQ);
@@ -262,23 +244,7 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[i] = 0u;
     }
-    if (valid) {
-      if constexpr (OUT_F32) {
-        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + out_row * D + c * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv_l, __uint_as_float(o[4 * i + 1]) * inv_l,
-                               __uint_as_float(o[4 * i + 2]) * inv_l, __uint_as_float(o[4 * i + 3]) * inv_l);
-      } else {
-        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + out_row * D + c * 32);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * inv_l, __uint_as_float(o[8 * i + 1]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * i + 2]) * inv_l, __uint_as_float(o[8 * i + 3]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * i + 4]) * inv_l, __uint_as_float(o[8 * i + 5]) * inv_l),
-                              pack_bf16(__uint_as_float(o[8 * i + 6]) * inv_l, __uint_as_float(o[8 * i + 7]) * inv_l));
-      }
-    }
+    if (valid) store_row32<OUT_F32>(p.out, out_row * D + c * 32, o, inv_l);
   }
   if (valid && p.lse != nullptr)
     p.lse[out_row] = l_run > 0.f ? m_run * 0.69314718055994531f + logf(l_run) : -INFINITY;
@@ -289,17 +255,21 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 template <int D, bool F32>
-int launch_typed(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p,
-                 int64_t n_tiles, cudaStream_t stream) {
+int launch_typed(const CUtensorMap* maps, const AttnParams& p, cudaStream_t stream) {
   auto kern = fga_attn_sync_kernel<D, F32>;
   const int smem = Smem<D>::ALLOC;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return check_launch("cudaFuncSetAttribute(attn)");
-  kern<<<static_cast<unsigned>(n_tiles), 128, smem, stream>>>(tq, tk, tv, p);
+  kern<<<static_cast<unsigned>(p.n_tiles), 128, smem, stream>>>(maps[0], maps[1], maps[2], p);
   return check_launch("fga_attn_sync_kernel");
 }
 
 }  // namespace
+
+int launch_attn_sync(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream) {
+  if (d == 64) return out_f32 ? launch_typed<64, true>(maps, p, stream) : launch_typed<64, false>(maps, p, stream);
+  return out_f32 ? launch_typed<128, true>(maps, p, stream) : launch_typed<128, false>(maps, p, stream);
+}
 
 int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
                 const int32_t* counts, void* o, int o_dtype, float* lse, const fga_shape& s, bool dense,
@@ -313,18 +283,24 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
   const int64_t n_tiles = B * H * G * tpg;
   if (n_tiles >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "too many tiles");
 
-  CUtensorMap tq, tk, tv;
+  // maps: Q (128-row box), K and V (1-row box for gather4), K and V (128-row box, dense path)
+  CUtensorMap maps[5];
   int rc;
-  if ((rc = make_tmap_bf16_2d(&tq, q, rows, D, 64, BM)) != FGA_OK) return rc;
-  if ((rc = make_tmap_bf16_2d(&tk, k, rows, D, 64, 1)) != FGA_OK) return rc;
-  if ((rc = make_tmap_bf16_2d(&tv, v, rows, D, 64, 1)) != FGA_OK) return rc;
+  if ((rc = make_tmap_bf16_2d(&maps[0], q, rows, D, 64, BM)) != FGA_OK) return rc;
+  if ((rc = make_tmap_bf16_2d(&maps[1], k, rows, D, 64, 1)) != FGA_OK) return rc;
+  if ((rc = make_tmap_bf16_2d(&maps[2], v, rows, D, 64, 1)) != FGA_OK) return rc;
+  if ((rc = make_tmap_bf16_2d(&maps[3], k, rows, D, 64, BN)) != FGA_OK) return rc;
+  if ((rc = make_tmap_bf16_2d(&maps[4], v, rows, D, 64, BN)) != FGA_OK) return rc;
 
   AttnParams p{};
+  p.k = k;
+  p.v = v;
   p.idx = idx;
   p.idx_group_stride = idx_group_stride;
   p.counts = counts;
   p.out = o;
   p.lse = lse;
+  p.n_tiles = n_tiles;
   p.heads = static_cast<int>(H);
   p.seq_len = static_cast<int>(N);
   p.group_size = static_cast<int>(M);
@@ -336,10 +312,9 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
   if (n_tiles == 0) return FGA_OK;
 
   const bool f32 = o_dtype == FGA_OUT_F32;
-  if (D == 64) return f32 ? launch_typed<64, true>(tq, tk, tv, p, n_tiles, stream)
-                          : launch_typed<64, false>(tq, tk, tv, p, n_tiles, stream);
-  return f32 ? launch_typed<128, true>(tq, tk, tv, p, n_tiles, stream)
-             : launch_typed<128, false>(tq, tk, tv, p, n_tiles, stream);
+  const char* which = std::getenv("FGA_ATTN_KERNEL");
+  if (which != nullptr && std::strcmp(which, "sync") == 0) return launch_attn_sync(maps, p, static_cast<int>(D), f32, stream);
+  return launch_attn_ws(maps, p, static_cast<int>(D), f32, stream);
 }
 
 }  // namespace fga

@@ -34,7 +34,11 @@ def timeit(fn, iters=10, flush=None):
 
 def main():
     B, H, N, D, M = 1, int(sys.argv[1]) if len(sys.argv) > 1 else 12, 32760, 128, 128
-    dens = float(sys.argv[2]) if len(sys.argv) > 2 else 0.45
+    for dens in ([float(sys.argv[2])] if len(sys.argv) > 2 else [0.45, 0.3, 0.2]):
+        run(B, H, N, D, M, dens)
+
+
+def run(B, H, N, D, M, dens):
     G = (N + M - 1) // M
     st = torch.cuda.current_stream().cuda_stream
     q, k, v = (torch.randn(B, H, N, D, device="cuda", dtype=torch.bfloat16) for _ in range(3))
