@@ -1,0 +1,497 @@
+#!/usr/bin/env python
+"""FG-Attn layer benchmark (BASELINE.json metric) -- one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2] [--density 0.45]
+
+Workload (config "c2", BASELINE.json configs[1]): one Wan 2.1 1.3B attention
+layer at 480p/81 frames -- B=1 per GPU, H=12, N=32760, D=128, M=128, bf16
+Q/K/V ~ N(0,1) (synthetic), a uniform-random M x 1 slice mask keeping exactly
+round(d*N) keys per query group (the random_mask count rule), d=0.45.
+
+A step is one sparse_attention call over the whole layer with inputs
+resident in HBM; L2 is flushed (512 MiB write) before every step, outside
+the timed events.  ``value`` = algorithmic TFLOP/s = 4*D*sum(rows_g*count_g)
+(perfmodel.py:104-105) / device time, summed over ranks.  Multi-GPU: one
+process per GPU (torchrun), every rank runs its own batch element of the
+layer (weak scaling, no collective on the hot path); NCCL is used only to
+take the max time over ranks and to all-gather an output sample for the
+bitwise cross-rank check.
+
+``e2e`` is the same metric through the public API from pinned HOST buffers:
+per step H2D of Q/K/V and the uint8 slice mask, K1b compaction, attention,
+D2H of O.  ``cpu_baseline`` (rank 0, N=1) times the oracle port of the
+reference sparse_attention on the host cores on a bounded sample of the
+same groups and doubles as the parity check of the GPU output.
+``--impl reference`` times only that CPU path (the reference arm).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+METRIC = "FG-attn layer latency ms, TFLOP/s & speedup vs dense at Wan2.1 480p/720p"
+
+CONFIGS = {
+    # name: (heads, seq_len, head_dim, group_size, description)
+    "c1": (2, 4096, 64, 128, "synthetic single-layer FG-attn, B=1, 2 heads, seq 4096, D=64"),
+    "c2": (12, 32760, 128, 128, "Wan2.1-1.3B attention layer, 480p/81 frames: 12 heads, seq 32760, D=128"),
+    "c3": (12, 75600, 128, 128, "Wan2.1-1.3B attention layer, 720p/81 frames: 12 heads, seq 75600, D=128"),
+    "c4": (40, 32760, 128, 128, "Wan2.1-14B attention layer, 480p: 40 heads, seq 32760, D=128"),
+    "c5": (40, 75600, 128, 128, "Wan2.1-14B attention layer, 720p: 40 heads, seq 75600, D=128"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--density", type=float, default=0.45)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-extras", action="store_true", help="skip dense/e2e/cpu legs (for ncu)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline work budget")
+    ap.add_argument("--cpu-worker", default=None, help=argparse.SUPPRESS)
+    return ap.parse_args()
+
+
+# ============================================================ CPU (oracle port) legs
+
+def _cpu_pool_main(workdir: str):
+    """Subprocess entry: OPENBLAS/OMP threads pinned to 1 before NumPy loads,
+    one process per core, each computing whole groups with the oracle."""
+    import multiprocessing as mp
+
+    with open(os.path.join(workdir, "job.json")) as f:
+        job = json.load(f)
+    cores = job["cores"]
+    ctx = mp.get_context("spawn")
+    tasks = [(workdir, i) for i in range(len(job["groups"]))]
+    with ctx.Pool(cores, initializer=_cpu_init, initargs=(workdir,)) as pool:
+        pool.map(_cpu_noop, range(cores * 2))  # import + mmap warm-up outside the timing
+        results = {}
+        t0 = time.perf_counter()
+        for rep in range(job["reps"]):
+            for i, out in pool.imap_unordered(_cpu_task, tasks, chunksize=1):
+                results[i] = out
+        elapsed = time.perf_counter() - t0
+    import numpy as np
+
+    np.save(os.path.join(workdir, "out.npy"), np.stack([results[i] for i in range(len(tasks))]))
+    with open(os.path.join(workdir, "timing.json"), "w") as f:
+        json.dump({"seconds": elapsed, "reps": job["reps"]}, f)
+
+
+_W = {}
+
+
+def _cpu_init(workdir):
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import oracle  # noqa: F401  (CPU-baseline leg: the only bench path that runs the oracle)
+
+    with open(os.path.join(workdir, "job.json")) as f:
+        _W["job"] = json.load(f)
+    for name in ("q", "k", "v", "idx", "counts"):
+        _W[name] = np.load(os.path.join(workdir, name + ".npy"), mmap_mode="r")
+
+
+def _cpu_noop(_):
+    return 0
+
+
+def _cpu_task(arg):
+    import numpy as np
+    import oracle
+
+    _, i = arg
+    job = _W["job"]
+    g = job["groups"][i]
+    m = job["group_size"]
+    lo, hi = g * m, min(g * m + m, job["seq_len"])
+    keys = np.asarray(_W["idx"][i, : int(_W["counts"][i])], dtype=np.int64)
+    out = oracle.sparse_attention_group(np.asarray(_W["q"][lo:hi]), _W["k"], _W["v"], keys, job["scale"])
+    full = np.zeros((m, _W["q"].shape[1]), np.float32)
+    full[: hi - lo] = out
+    return i, full
+
+
+def run_cpu_baseline(qh, kh, vh, idx_rows, counts, groups, group_size, scale, cores, reps=1):
+    """Time the oracle port on ``cores`` host processes.  Returns (seconds, outputs)."""
+    import numpy as np
+
+    workdir = tempfile.mkdtemp(prefix="fga_cpu_")
+    np.save(os.path.join(workdir, "q.npy"), qh)
+    np.save(os.path.join(workdir, "k.npy"), kh)
+    np.save(os.path.join(workdir, "v.npy"), vh)
+    np.save(os.path.join(workdir, "idx.npy"), idx_rows)
+    np.save(os.path.join(workdir, "counts.npy"), counts)
+    with open(os.path.join(workdir, "job.json"), "w") as f:
+        json.dump({"groups": [int(g) for g in groups], "group_size": group_size, "seq_len": int(qh.shape[0]),
+                   "scale": float(scale), "cores": cores, "reps": reps}, f)
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               CUDA_VISIBLE_DEVICES="")
+    subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-worker", workdir], check=True, env=env)
+    with open(os.path.join(workdir, "timing.json")) as f:
+        t = json.load(f)
+    return t["seconds"], np.load(os.path.join(workdir, "out.npy"))
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_arm(args):
+    """--impl reference: the oracle port of the reference sparse_attention on the
+    host cores, same metric/config, rank 0 only."""
+    import numpy as np
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, ROOT)
+    import oracle
+
+    heads, n, d, m, desc = CONFIGS[args.config]
+    cores = host_cores()
+    qh = oracle.bf16_round(oracle.gaussian((n, d), 1))
+    kh = oracle.bf16_round(oracle.gaussian((n, d), 2))
+    vh = oracle.bf16_round(oracle.gaussian((n, d), 3))
+    g_count = -(-n // m)
+    count = max(1, round(args.density * n))
+    rng = np.random.Generator(np.random.Philox(args.seed))   # random_mask count rule (sparse.py:216-232)
+    per_step = max(1, cores)
+    groups = [int(x) % g_count for x in range(per_step)]
+    idx = np.stack([np.sort(rng.choice(n, size=count, replace=False)) for _ in groups]).astype(np.int32)
+    counts = np.full(len(groups), count, np.int32)
+    rows = np.array([min(m, n - g * m) for g in groups])
+    flops_step = int(4 * d * (rows * count).sum())
+    total = args.warmup + args.steps
+    secs, _ = run_cpu_baseline(qh, kh, vh, idx, counts, groups, m, 1 / math.sqrt(d), cores, reps=total)
+    per = secs / total
+    value = flops_step / per / 1e12
+    sample = (f"{per_step} query groups of head 0 per step ({count} keys each, {m} rows), "
+              f"{total} steps timed together incl. {args.warmup} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": desc, "heads": heads, "seq_len": n, "head_dim": d, "group_size": m,
+                   "density": args.density, "keys_per_group": count},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ============================================================ GPU helpers
+
+class ClockSampler:
+    """NVML polling (10 ms) of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x4: "sw_power_cap", 0x1: "gpu_idle",
+               0x2: "applications_clocks_setting"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), p["hbm_gbs"], "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config, density):
+    """Per-launch dram bytes of the attention kernel from the committed ncu capture, if it matches."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        e = d.get(f"{config}@{density}")
+        return None if e is None else e["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def timed_steps(torch, fn, steps, flush, stream):
+    """Per-step CUDA-event times (ms) on ``stream``; L2 flushed before each step, untimed."""
+    ts = []
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        ts.append((a, b))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ts]
+
+
+# ============================================================ our arm
+
+def ours(args):
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    sys.path.insert(0, ROOT)
+    import paper_2509_16518_b200 as fga
+    from paper_2509_16518_b200 import _lib
+
+    lib = _lib.load()
+    heads, n, d, m, desc = CONFIGS[args.config]
+    cfg = fga.AttnConfig(1, heads, n, d, group_size=m, precision="bf16")
+    stream = torch.cuda.current_stream()
+    gen = torch.Generator(device=dev).manual_seed(1234 + args.seed)   # identical on every rank (bitwise check)
+    q = torch.randn(cfg.dims, device=dev, dtype=torch.float32, generator=gen).to(torch.bfloat16)
+    k = torch.randn(cfg.dims, device=dev, dtype=torch.float32, generator=gen).to(torch.bfloat16)
+    v = torch.randn(cfg.dims, device=dev, dtype=torch.float32, generator=gen).to(torch.bfloat16)
+    count = max(1, round(args.density * n))
+    rows_g = cfg.batch * cfg.heads * cfg.num_groups
+    keep = torch.empty((1, heads, cfg.num_groups, n), dtype=torch.uint8, device=dev)
+    _lib.call("fga_random_keep", rows_g, n, count, 77 + args.seed, keep.data_ptr(), stream.cuda_stream)
+    mask = fga.compact_keep(keep, m)
+    rep = fga.count_flops(cfg, mask)
+    flops = rep.flops_matmul           # 4*D*pairs: the roofline numerator (softmax excluded)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        return fga.sparse_attention(q, k, v, mask, cfg)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    with ClockSampler(local) as clk:
+        times = timed_steps(torch, step, args.steps, flush, stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    kernel_ms = sum(times) / len(times)
+    if dist:
+        t = torch.tensor([kernel_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        kernel_ms = float(t.item())
+    out = step()
+    torch.cuda.synchronize()
+
+    peak, peak_sus, hbm_peak, peak_src = measured_peaks()
+    achieved = flops / (kernel_ms * 1e-3) / 1e12
+    value = achieved * world
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": kernel_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (N(0,1) bf16 Q/K/V, uniform random slice mask)",
+        "config": {"workload": desc, "config": args.config, "batch_per_gpu": 1, "global_batch": world,
+                   "heads": heads, "seq_len": n, "head_dim": d, "group_size": m, "density": args.density,
+                   "keys_per_group": count, "parallelism": f"dp{world} (batch-sharded, weak)",
+                   "l2": "flushed between steps (512 MiB write, untimed)"},
+        "latency_ms": kernel_ms,
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "frac_of_sustained": achieved / peak_sus if peak_sus else None,
+                     "peak_source": peak_src, "traffic": ncu_traffic(args.config, args.density),
+                     "algorithmic_flops_per_launch": flops,
+                     "gathered_kv_bytes_per_launch": int(rep.density * cfg.batch * heads * cfg.num_groups * n) * 4 * d,
+                     "kernel": "fga_attn_ws_kernel"},
+        "clocks": clk.summary(),
+        "wall_s_timed_region": wall,
+    }
+
+    # ---- validation all-gather (NCCL, outside the timed region): bitwise equal across ranks
+    if dist:
+        from paper_2509_16518_b200.shard import gather_outputs
+
+        sample = out[0, 0, :256].contiguous()
+        allo = gather_outputs(sample)
+        line["cross_rank_bitwise_equal"] = bool(all(torch.equal(allo[0], allo[r]) for r in range(world)))
+
+    if not args.no_extras and rank == 0:
+        extras(args, torch, np, fga, _lib, cfg, q, k, v, keep, mask, out, flops, flush, stream, line, world,
+               hbm_peak, peak_src, count)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def extras(args, torch, np, fga, _lib, cfg, q, k, v, keep, mask, out, flops, flush, stream, line, world,
+           hbm_peak, peak_src, count):
+    heads, n, d, m = cfg.heads, cfg.seq_len, cfg.head_dim, cfg.group_size
+    kernel_ms = line["ms_per_step"]
+    # ---- dense denominators on the same GPU: our dense kernel + torch SDPA backends
+    dense = {}
+    t_own = timed_steps(torch, lambda: fga.flash_attention(q, k, v, cfg), max(3, args.steps // 2), flush, stream)
+    dense["own_tcgen05_ms"] = sorted(t_own)[len(t_own) // 2]
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+
+    for name, be in (("sdpa_cudnn_ms", SDPBackend.CUDNN_ATTENTION), ("sdpa_flash_ms", SDPBackend.FLASH_ATTENTION),
+                     ("sdpa_efficient_ms", SDPBackend.EFFICIENT_ATTENTION)):
+        try:
+            with sdpa_kernel([be]):
+                torch.nn.functional.scaled_dot_product_attention(q, k, v)
+                tt = timed_steps(torch, lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v),
+                                 max(3, args.steps // 2), flush, stream)
+            dense[name] = sorted(tt)[len(tt) // 2]
+        except Exception as e:  # backend not available for this shape
+            dense[name] = None
+    best = min(x for x in dense.values() if x)
+    dense["best_ms"] = best
+    dense["dense_flops"] = 4 * d * heads * n * n
+    line["dense"] = dense
+    line["speedup_vs_dense"] = best / kernel_ms
+
+    # ---- K1b compaction (HBM-bound): keep bytes read + 4*count written (+ counts)
+    t_c = timed_steps(torch, lambda: fga.compact_keep(keep, m), max(3, args.steps), flush, stream)
+    c_ms = sum(t_c) / len(t_c)
+    c_bytes = keep.numel() + 4 * int(mask.counts.sum().item()) + 4 * mask.counts.numel()
+    line["mask_build"] = {"kernel": "fga_compact_kernel", "ms": c_ms, "bytes": c_bytes,
+                          "achieved_gbs": c_bytes / (c_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                          "frac": c_bytes / (c_ms * 1e-3) / 1e9 / hbm_peak, "peak_source": peak_src,
+                          "layer_ms_incl_compaction": kernel_ms + c_ms}
+
+    # ---- e2e through the public API from pinned host buffers
+    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+    hkeep = keep.cpu().pin_memory()
+    hout = torch.empty(cfg.dims, dtype=torch.bfloat16).pin_memory()
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    dkeep = torch.empty_like(keep)
+
+    def e2e_step():
+        dq.copy_(hq, non_blocking=True)
+        dk.copy_(hk, non_blocking=True)
+        dv.copy_(hv, non_blocking=True)
+        dkeep.copy_(hkeep, non_blocking=True)
+        mk = fga.compact_keep(dkeep, m)
+        o = fga.sparse_attention(dq, dk, dv, mk, cfg)
+        hout.copy_(o, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    t_e = timed_steps(torch, e2e_step, max(3, args.steps // 2), flush, stream)
+    e_ms = sum(t_e) / len(t_e)
+    h2d = 3 * q.numel() * 2 + keep.numel()
+    line["e2e"] = {"value": flops / (e_ms * 1e-3) / 1e12 * world, "unit": "TFLOP/s", "ms_per_step": e_ms,
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": out.numel() * 2,
+                   "path": "pinned host Q/K/V + uint8 slice mask -> compact_keep -> sparse_attention -> host O"}
+
+    # ---- CPU baseline (oracle port, rank 0, N=1 only) + parity of the same groups
+    if world == 1:
+        cores = host_cores()
+        n_groups = cfg.num_groups
+        per_group_s = 4 * d * m * count / 25e9      # ~25 GFLOP/s per core for the NumPy port
+        budget = max(cores, int(args.cpu_seconds * cores / per_group_s))
+        sample_groups = list(range(min(n_groups, budget)))
+        qh = q[0, 0].float().cpu().numpy()
+        kh = k[0, 0].float().cpu().numpy()
+        vh = v[0, 0].float().cpu().numpy()
+        idx_rows = mask.idx[0, 0, sample_groups].cpu().numpy()
+        cnts = mask.counts[0, 0, sample_groups].cpu().numpy()
+        secs, cpu_out = run_cpu_baseline(qh, kh, vh, idx_rows, cnts, sample_groups, m, cfg.scale, cores)
+        rows = np.array([min(m, n - g * m) for g in sample_groups])
+        f_sample = int(4 * d * (rows * cnts.astype(np.int64)).sum())
+        cpu_val = f_sample / secs / 1e12
+        gpu_rows = out[0, 0].float().cpu().numpy()
+        err = 0.0
+        for j, g in enumerate(sample_groups):
+            lo, hi = g * m, min(g * m + m, n)
+            err = max(err, float(np.abs(gpu_rows[lo:hi] - cpu_out[j, : hi - lo]).max()))
+        line["cpu_baseline"] = {"value": cpu_val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                                "sample": f"{len(sample_groups)} query groups of head 0 ({count} keys each), "
+                                          f"oracle.sparse_attention_group, one process per core",
+                                "seconds": secs, "gpu_vs_cpu_ratio": line["value"] / cpu_val}
+        line["parity"] = {"max_abs_err_vs_oracle": err, "tolerance": 2e-2, "groups_checked": len(sample_groups),
+                          "output_dtype": "bf16"}
+
+
+def main():
+    args = parse()
+    if args.cpu_worker:
+        _cpu_pool_main(args.cpu_worker)
+        return
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    ours(args)
+
+
+if __name__ == "__main__":
+    main()

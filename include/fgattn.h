@@ -89,6 +89,17 @@ int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32
                         fga_shape shape, void* stream);
 
 /*
+ * fga_sparse_attn_fwd restricted to work tiles [tile_begin, tile_end).  A
+ * tile is <=128 query rows of one group; tiles are numbered head-major,
+ * tile = ((b*H + h)*G + g)*ceil(M/128) + sub, so a contiguous range is a run
+ * of (head, group-range) units.  Multi-GPU shards call this with their own
+ * range on full-size tensors; rows outside the range are not written.
+ */
+int fga_sparse_attn_fwd_tiles(const void* q, const void* k, const void* v, const int32_t* idx,
+                              int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
+                              fga_shape shape, int64_t tile_begin, int64_t tile_end, void* stream);
+
+/*
  * Dense attention with the same kernel and contiguous key chunks (every group
  * lists all N keys).  Replaces tiled.py:80-114 (flash_attention) /
  * oracle.py:29-42 (dense_attention); the dense denominator of the speed-up.
@@ -127,13 +138,24 @@ int fga_threshold_keep(const float* scores, int64_t n_elems, float tau, uint8_t*
 int fga_topk_keep(const float* scores, int64_t rows, int64_t n, int64_t top_k, uint8_t* keep, void* stream);
 
 /*
+ * Group maximum of an explicit post-softmax map (K1a, cached builder from a
+ * materialised map).  Replaces masks.py:66-72 (_group_max) on
+ * analysis_scores(map) as used by masks.py:94-105 (build_mask_cached):
+ *   gmax[bh, g, j] = max_{i in group g} map[bh, i, j]   (bf16-rounded when round_bf16)
+ *   map  : fp32 [BH, N, N];  gmax : fp32 [BH, G, N].
+ */
+int fga_group_max_map(const float* map, int64_t bh, int64_t n, int64_t group_size, int round_bf16, float* gmax,
+                      void* stream);
+
+/*
  * Cached-threshold statistics (K1a, cached builder) without materialising
  * the [B,H,N,N] map: pass 1 computes each query row's softmax normaliser,
  * pass 2 the per-group column maximum of the normalised map.  Replaces
  * oracle.py:45-52 (attention_map) + masks.py:66-72 (_group_max) as used by
  * masks.py:94-105 (build_mask_cached).
  *   gmax   : fp32 [B, H, G, N]; bf16-rounded when round_bf16 != 0.
- *   row_ws : fp32 workspace of 2*B*H*N floats (row max, row denominator).
+ *   row_ws : fp32 workspace of at least B*H*N floats (row maxima); the fp64
+ *            row denominators use a stream-ordered temporary allocation.
  */
 int fga_cached_group_max(const void* q, const void* k, fga_shape shape, int round_bf16, float* gmax,
                          float* row_ws, void* stream);

@@ -1,0 +1,24 @@
+"""B200-native FG-Attn: fine-grained (M x 1 slice) sparse attention.
+
+Drop-in for the operator API of the reference package ``sliceattn``
+(arXiv 2509.16518): same names, signatures, defaults and exceptions, with the
+work done by hand-written sm_100a kernels in ``libfgattn.so`` (see
+include/fgattn.h).  There is no CPU fallback.
+
+    from paper_2509_16518_b200 import AttnConfig, new_tensor, random_mask, sparse_attention
+    cfg = AttnConfig(1, 2, 4096, 64, precision="bf16")
+    q, k, v = (new_tensor(cfg, "gaussian", seed=s) for s in (1, 2, 3))
+    out = sparse_attention(q, k, v, random_mask(cfg, 0.3, seed=0), cfg)
+"""
+
+from .core import (GATHER, PRECISIONS, STREAM, AttnConfig, AttnMap, AttnTensor, NumericError, ShapeError,
+                   TileEvent, analysis_scores, ingest, make_rng, new_tensor, round_bf16)
+from .masks import (STRATEGIES, CachedMaskState, MaskBuilderConfig, build_mask, build_mask_avg_query,
+                    build_mask_cached, build_mask_cached_qk, cached_group_max, pooled_query_scores, refresh_policy)
+from .perfmodel import CostReport, count_flops, flop_speedup, synthetic_trace, trace_flops
+from .sparse import (DeviceIndexMask, PackedTile, SparseIndexMask, compact_keep, export_padded, full_mask,
+                     gather_rows, import_padded, mask_density, mask_jaccard, masked_dense_attention, random_mask,
+                     random_mask_device, sparse_attention)
+from .tiled import dense_attention, flash_attention
+
+__version__ = "0.1.0"

@@ -35,11 +35,13 @@ _SIGS = {
     "fga_device_supported": ([_I], _I),
     "fga_compact": ([_P, _P, _I64, _I64, _P, _I64, _P, _I, _P], _I),
     "fga_sparse_attn_fwd": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _P], _I),
+    "fga_sparse_attn_fwd_tiles": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _I64, _I64, _P], _I),
     "fga_dense_attn_fwd": ([_P, _P, _P, _P, _I, _P, FgaShape, _P], _I),
     "fga_gather_rows": ([_P, _I64, _I64, _P, _I64, _P, _P], _I),
     "fga_pooled_scores": ([_P, _P, FgaShape, _I, _P, _P], _I),
     "fga_threshold_keep": ([_P, _I64, _F, _P, _P], _I),
     "fga_topk_keep": ([_P, _I64, _I64, _I64, _P, _P], _I),
+    "fga_group_max_map": ([_P, _I64, _I64, _I64, _I, _P, _P], _I),
     "fga_cached_group_max": ([_P, _P, FgaShape, _I, _P, _P, _P], _I),
     "fga_random_keep": ([_I64, _I64, _I64, ctypes.c_uint64, _P, _P], _I),
 }

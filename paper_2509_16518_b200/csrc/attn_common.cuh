@@ -22,7 +22,8 @@ struct AttnParams {
   const int32_t* counts;
   void* out;
   float* lse;
-  int64_t n_tiles;
+  int64_t tile_begin;  // first tile of this launch (multi-GPU shards run tile ranges)
+  int64_t n_tiles;     // one past the last tile
   int heads, seq_len, group_size, groups, tiles_per_group;
   float scale_log2;
   int dense;

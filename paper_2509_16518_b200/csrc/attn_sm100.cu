@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(128, 1)
   const int warp = tid >> 5;
   const int lane = tid & 31;
 
-  const Tile tl = decode_tile(p, blockIdx.x);
+  const Tile tl = decode_tile(p, p.tile_begin + blockIdx.x);
   const int q0 = tl.q0, rows = tl.rows, row0 = tl.row0, count = tl.count, nchunks = tl.nchunks;
   const int32_t* list = tl.list;
 
@@ -260,7 +260,7 @@ int launch_typed(const CUtensorMap* maps, const AttnParams& p, cudaStream_t stre
   const int smem = Smem<D>::ALLOC;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return check_launch("cudaFuncSetAttribute(attn)");
-  kern<<<static_cast<unsigned>(p.n_tiles), 128, smem, stream>>>(maps[0], maps[1], maps[2], p);
+  kern<<<static_cast<unsigned>(p.n_tiles - p.tile_begin), 128, smem, stream>>>(maps[0], maps[1], maps[2], p);
   return check_launch("fga_attn_sync_kernel");
 }
 
@@ -273,7 +273,7 @@ int launch_attn_sync(const CUtensorMap* maps, const AttnParams& p, int d, bool o
 
 int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
                 const int32_t* counts, void* o, int o_dtype, float* lse, const fga_shape& s, bool dense,
-                cudaStream_t stream) {
+                cudaStream_t stream, int64_t tile_begin, int64_t tile_end) {
   const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
   if (D != 64 && D != 128) return fail(FGA_EUNSUPPORTED, "head_dim must be 64 or 128");
   const int64_t rows = B * H * N;
@@ -282,6 +282,9 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
   const int64_t tpg = (M + BM - 1) / BM;
   const int64_t n_tiles = B * H * G * tpg;
   if (n_tiles >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "too many tiles");
+  if (tile_end < 0) tile_end = n_tiles;
+  if (tile_begin < 0 || tile_begin > tile_end || tile_end > n_tiles)
+    return fail(FGA_EINVAL, "tile range must satisfy 0 <= begin <= end <= B*H*G*ceil(M/128)");
 
   // maps: Q (128-row box), K and V (1-row box for gather4), K and V (128-row box, dense path)
   CUtensorMap maps[5];
@@ -300,7 +303,8 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
   p.counts = counts;
   p.out = o;
   p.lse = lse;
-  p.n_tiles = n_tiles;
+  p.tile_begin = tile_begin;
+  p.n_tiles = tile_end;
   p.heads = static_cast<int>(H);
   p.seq_len = static_cast<int>(N);
   p.group_size = static_cast<int>(M);
@@ -309,7 +313,7 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
   const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
   p.scale_log2 = scale * 1.4426950408889634f;
   p.dense = dense ? 1 : 0;
-  if (n_tiles == 0) return FGA_OK;
+  if (tile_end == tile_begin) return FGA_OK;
 
   const bool f32 = o_dtype == FGA_OUT_F32;
   const char* which = std::getenv("FGA_ATTN_KERNEL");

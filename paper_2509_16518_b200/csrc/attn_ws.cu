@@ -144,7 +144,7 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
   const uint32_t kv_base = smem_u32(smem + L::OFF_KV);
   uint32_t item = 0;
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
     const int qs = it & 1;
     if (pw == 0) {
@@ -223,7 +223,7 @@ __device__ __forceinline__ void mma_issuer(const AttnParams& p, uint8_t* smem, c
   const uint32_t smem_q = smem_u32(smem + L::OFF_Q);
   uint32_t chunk = 0;
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
     const int qs = it & 1, ob = it & 1;
     const uint32_t tO = tmem + 256 + ob * 128;
@@ -278,7 +278,7 @@ __device__ __forceinline__ void softmax_wg(const AttnParams& p, const Bars& bar,
   const float sl2 = p.scale_log2;
   uint32_t chunk = 0;
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
     const int ob = it & 1;
     const uint32_t tO = tmem + 256 + ob * 128 + lane_off;
@@ -447,7 +447,8 @@ int launch_ws(const CUtensorMap* maps, const AttnParams& p, cudaStream_t stream)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t grid = p.n_tiles < sms ? p.n_tiles : sms;
+  const int64_t span = p.n_tiles - p.tile_begin;
+  const int64_t grid = span < sms ? span : sms;
   kern<<<static_cast<unsigned>(grid), 32 * (5 + NPROD), smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
   return check_launch("fga_attn_ws_kernel");
 }

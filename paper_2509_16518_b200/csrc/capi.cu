@@ -9,6 +9,7 @@ namespace fga {
 
 int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, float* scores, cudaStream_t st);
 int launch_threshold(const float* s, int64_t n, float tau, uint8_t* keep, cudaStream_t st);
+int launch_group_max_map(const float* map, int64_t bh, int64_t n, int64_t m, int round, float* gmax, cudaStream_t st);
 int launch_topk(const float* s, int64_t rows, int64_t n, int64_t k, uint8_t* keep, cudaStream_t st);
 int launch_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, uint8_t* keep, cudaStream_t st);
 int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, float* ws,
@@ -108,6 +109,18 @@ int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32
                      static_cast<cudaStream_t>(stream));
 }
 
+int fga_sparse_attn_fwd_tiles(const void* q, const void* k, const void* v, const int32_t* idx,
+                              int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
+                              fga_shape shape, int64_t tile_begin, int64_t tile_end, void* stream) {
+  int rc = check_shape(shape);
+  if (rc != FGA_OK) return rc;
+  if (!q || !k || !v || !idx || !counts || !o) return fail(FGA_EINVAL, "null pointer");
+  if (idx_group_stride < 1) return fail(FGA_EINVAL, "idx_group_stride must be >= 1");
+  if (o_dtype != FGA_OUT_BF16 && o_dtype != FGA_OUT_F32) return fail(FGA_EINVAL, "o_dtype must be FGA_OUT_BF16 or FGA_OUT_F32");
+  return launch_attn(q, k, v, idx, idx_group_stride, counts, o, o_dtype, lse, shape, false,
+                     static_cast<cudaStream_t>(stream), tile_begin, tile_end);
+}
+
 int fga_dense_attn_fwd(const void* q, const void* k, const void* v, void* o, int o_dtype, float* lse,
                        fga_shape shape, void* stream) {
   int rc = check_shape(shape);
@@ -140,6 +153,12 @@ int fga_topk_keep(const float* scores, int64_t rows, int64_t n, int64_t top_k, u
   if (rows < 0 || n < 1) return fail(FGA_EINVAL, "rows must be >= 0 and n >= 1");
   if (rows > 0 && (!scores || !keep)) return fail(FGA_EINVAL, "null pointer");
   return launch_topk(scores, rows, n, top_k, keep, static_cast<cudaStream_t>(stream));
+}
+
+int fga_group_max_map(const float* map, int64_t bh, int64_t n, int64_t group_size, int round_bf16, float* gmax,
+                      void* stream) {
+  if (!map || !gmax) return fail(FGA_EINVAL, "null pointer");
+  return launch_group_max_map(map, bh, n, group_size, round_bf16, gmax, static_cast<cudaStream_t>(stream));
 }
 
 int fga_cached_group_max(const void* q, const void* k, fga_shape shape, int round_bf16, float* gmax, float* row_ws,

@@ -24,7 +24,7 @@ int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_
 // Launchers (attn_sm100.cu / gather.cu / compact.cu / maskbuild.cu).
 int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
                 const int32_t* counts, void* o, int o_dtype, float* lse, const fga_shape& s, bool dense,
-                cudaStream_t stream);
+                cudaStream_t stream, int64_t tile_begin = 0, int64_t tile_end = -1);
 int launch_gather(const void* matrix, int64_t rows, int64_t d, const int32_t* indices, int64_t n_idx, void* out,
                   cudaStream_t stream);
 int launch_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t n, int32_t* idx,

@@ -102,6 +102,20 @@ __global__ void __launch_bounds__(256) pooled_scores_kernel(const float* __restr
   }
 }
 
+// ------------------------------------------------------------ group max of an explicit map
+__global__ void group_max_map_kernel(const float* __restrict__ map, int64_t n, int64_t m, int64_t g_count,
+                                     int round, float* __restrict__ gmax) {
+  const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t g = blockIdx.y, bh = blockIdx.z;
+  if (j >= n) return;
+  const int64_t lo = g * m, hi = lo + m < n ? lo + m : n;
+  const float* col = map + bh * n * n + j;
+  float best = -INFINITY;
+  for (int64_t i = lo; i < hi; ++i) best = fmaxf(best, col[i * n]);
+  if (round) best = bf16_rne(best);
+  gmax[(bh * g_count + g) * n + j] = best;
+}
+
 // ------------------------------------------------------------ threshold
 __global__ void threshold_kernel(const float* __restrict__ s, int64_t n, float tau, uint8_t* __restrict__ keep) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
@@ -326,6 +340,16 @@ int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int r
   int rc = check_launch("pooled_scores_kernel");
   cudaFreeAsync(qbar, st);
   return rc;
+}
+
+int launch_group_max_map(const float* map, int64_t bh, int64_t n, int64_t m, int round, float* gmax,
+                         cudaStream_t st) {
+  if (bh < 1 || n < 1 || m < 1 || m > n) return fail(FGA_EINVAL, "group_max_map: bad shape");
+  const int64_t g = (n + m - 1) / m;
+  if (g > 65535 || bh > 65535) return fail(FGA_EINVAL, "group_max_map: too many groups or heads");
+  dim3 grid(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(g), static_cast<unsigned>(bh));
+  group_max_map_kernel<<<grid, 256, 0, st>>>(map, n, m, g, round, gmax);
+  return check_launch("group_max_map_kernel");
 }
 
 int launch_threshold(const float* s, int64_t n, float tau, uint8_t* keep, cudaStream_t st) {
