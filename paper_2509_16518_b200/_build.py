@@ -42,6 +42,24 @@ def _stale(out: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Development A/B build: all sources with extra -D flags -> build/variants/lib<name>.so."""
+    out_dir = os.path.join(BUILD, "variants", name)
+    os.makedirs(out_dir, exist_ok=True)
+    cc = nvcc()
+    objs = []
+    for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
+        obj = os.path.join(out_dir, os.path.basename(src)[:-3] + ".o")
+        r = subprocess.run([cc, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(r.stderr)
+        objs.append(obj)
+    lib = os.path.join(BUILD, "variants", f"lib{name}.so")
+    subprocess.run([cc, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs], check=True)
+    return lib
+
+
 def build(force: bool = False, verbose: bool = True) -> str:
     os.makedirs(BUILD, exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))

@@ -13,7 +13,7 @@ import os
 from .errors import ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfgattn.so")
+LIB_PATH = os.environ.get("FGA_LIB") or os.path.join(_HERE, "libfgattn.so")  # FGA_LIB: A/B builds
 
 FGA_OK, FGA_EINVAL, FGA_ERANGE, FGA_ECUDA, FGA_EUNSUPPORTED = 0, -1, -2, -3, -4
 FGA_OUT_BF16, FGA_OUT_F32 = 0, 1

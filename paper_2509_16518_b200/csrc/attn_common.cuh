@@ -27,7 +27,16 @@ struct AttnParams {
   int heads, seq_len, group_size, groups, tiles_per_group;
   float scale_log2;
   int dense;
+  long long* trace;  // debug timeline (FGA_TRACE=<file>): CTA 0, first tile, clock64 per phase
 };
+
+// Debug timeline hook: slot s of chunk j (j < 64) for CTA 0's first tile.
+#define FGA_TRACE_SLOTS 16
+#define FGA_TS(p, it, j, slot)                                                                         \
+  do {                                                                                                  \
+    if ((p).trace != nullptr && blockIdx.x == 0 && (it) == 0 && (j) < 64)                               \
+      (p).trace[(j) * FGA_TRACE_SLOTS + (slot)] = clock64();                                            \
+  } while (0)
 
 // One work tile: <=128 query rows of group (b,h,g) and that group's key list.
 struct Tile {

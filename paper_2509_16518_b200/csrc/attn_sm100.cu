@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "attn_common.cuh"
@@ -316,7 +317,27 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
   if (tile_end == tile_begin) return FGA_OK;
 
   const bool f32 = o_dtype == FGA_OUT_F32;
+  const char* trace_file = std::getenv("FGA_TRACE");
+  if (trace_file != nullptr && cudaMalloc(&p.trace, 64 * FGA_TRACE_SLOTS * sizeof(long long)) == cudaSuccess)
+    cudaMemsetAsync(p.trace, 0, 64 * FGA_TRACE_SLOTS * sizeof(long long), stream);
   const char* which = std::getenv("FGA_ATTN_KERNEL");
+  if (p.trace != nullptr) {
+    int rc2 = (which != nullptr && std::strcmp(which, "sync") == 0)
+                  ? launch_attn_sync(maps, p, static_cast<int>(D), f32, stream)
+                  : launch_attn_ws(maps, p, static_cast<int>(D), f32, stream);
+    long long host[64 * FGA_TRACE_SLOTS];
+    cudaMemcpyAsync(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    cudaFree(p.trace);
+    if (FILE* f = std::fopen(trace_file, "w")) {
+      for (int j = 0; j < 64; ++j) {
+        for (int k = 0; k < FGA_TRACE_SLOTS; ++k) std::fprintf(f, "%lld ", host[j * FGA_TRACE_SLOTS + k]);
+        std::fprintf(f, "\n");
+      }
+      std::fclose(f);
+    }
+    return rc2;
+  }
   if (which != nullptr && std::strcmp(which, "sync") == 0) return launch_attn_sync(maps, p, static_cast<int>(D), f32, stream);
   return launch_attn_ws(maps, p, static_cast<int>(D), f32, stream);
 }

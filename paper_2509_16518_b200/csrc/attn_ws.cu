@@ -8,8 +8,8 @@
 //
 // Roles (one CTA per SM, persistent, tiles strided over the grid):
 //   warps 0-3       softmax + epilogue: thread t owns query row t = TMEM lane t
-//   warp  4         MMA issuer (one thread): S_c = Q K_c^T (SS) into S[c%2],
-//                   then O += P_{c-1} V_{c-1} (TS: P read from TMEM)
+//   warp  4         MMA issuer (one warp, elected lane): S_c = Q K_c^T (SS)
+//                   into S[c%2], then O += P_{c-1} V_{c-1} (TS: P from TMEM)
 //   warps 5..5+NP-1 producers: Q by 2D TMA; each K/V chunk (one ring item of
 //                   128 rows) is packed into a 128B-swizzled slot -- the first
 //                   G4 rows by TMA tile::gather4, the rest by 16-byte cp.async
@@ -19,7 +19,8 @@
 //                   cp.async scales with producer warps (~8.2 TB/s at 16), so
 //                   the wide cp.async producer carries the gather and the TMA
 //                   unit adds an independent share.
-// Registers are rebalanced with setmaxnreg: softmax 232, everything else 56.
+// Registers are rebalanced with setmaxnreg: softmax 232, everything else 48
+// (.inc only draws from what the CTA released: see the static_assert).
 // TMEM (512 cols): S0 | S1 | O0 | O1.  P_c (bf16) overwrites S[c%2] cols 0-63.
 // Issue order S_0, S_1, PV_0, S_2, PV_1, ... gives softmax(c) the window
 // PV_{c-1} + S_{c+1} to run while the tensor core stays busy.
@@ -37,11 +38,16 @@
 namespace fga {
 namespace {
 
-constexpr int WARP_MMA = 4;
-constexpr int WARP_PROD0 = 5;
+constexpr int NSOFT = 4;  // softmax warps (one warpgroup: thread t owns row t)
+constexpr int WARP_MMA = NSOFT;
+constexpr int WARP_PROD0 = NSOFT + 1;
 constexpr int REG_SOFTMAX = 232;
-constexpr int REG_OTHER = 56;
+constexpr int REG_OTHER = 48;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units (factor 256)
+#ifndef FGA_EMU_EVERY
+#define FGA_EMU_EVERY (1 << 20)
+#endif
+constexpr int EMU_EVERY = FGA_EMU_EVERY;   // 1 in EMU_EVERY exp2 pairs on the FMA pipe
 
 template <int D>
 struct WsSmem {
@@ -52,7 +58,7 @@ struct WsSmem {
   static constexpr int OFF_BAR = OFF_KV + NSLOT * KV;
   static constexpr int NBAR = 2 + 2 + 2 * NSLOT + 2 + 2 + 1 + 2 + 2;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
-  static constexpr int ALLOC = BYTES + 1024;
+  static constexpr int ALLOC = BYTES;  // extern smem is declared __align__(1024)
 };
 
 struct Bars {
@@ -213,14 +219,18 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
   }
 }
 
-// ------------------------------------------------------------------ MMA issuer (one thread)
+// ------------------------------------------------------------------ MMA issuer (one warp)
+// The whole warp runs the loop (waits, descriptor arithmetic stay warp-uniform);
+// one elected lane issues each batch of tcgen05.mma + commits.
 template <int D>
 __device__ __forceinline__ void mma_issuer(const AttnParams& p, uint8_t* smem, const Bars& bar, uint32_t tmem) {
   using L = WsSmem<D>;
   constexpr uint32_t IDESC_S = idesc_bf16(BM, BN, false, false);  // Q, K both K-major
   constexpr uint32_t IDESC_O = idesc_bf16(BM, D, false, true);    // P from TMEM, V MN-major
-  const uint32_t smem_kv = smem_u32(smem + L::OFF_KV);
-  const uint32_t smem_q = smem_u32(smem + L::OFF_Q);
+  // descriptor templates; the start-address field (addr >> 4) is advanced by adding offset >> 4
+  const uint64_t dq0 = sdesc_sw128(smem_u32(smem + L::OFF_Q), 16, 1024);
+  const uint64_t dk0 = sdesc_sw128(smem_u32(smem + L::OFF_KV), 16, 1024);
+  const uint64_t dv0 = sdesc_sw128(smem_u32(smem + L::OFF_KV), HALF, 1024);
   uint32_t chunk = 0;
   int it = 0;
   for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
@@ -230,42 +240,58 @@ __device__ __forceinline__ void mma_issuer(const AttnParams& p, uint8_t* smem, c
     mbar_wait(&bar.q_full[qs], (it >> 1) & 1);
     mbar_wait(&bar.o_empty[ob], ((it >> 1) & 1) ^ 1);
     tc_fence_after();
-    const uint32_t qaddr = smem_q + qs * L::KV;
+    const uint64_t dq = dq0 + ((qs * L::KV) >> 4);
     for (int j = 0; j <= t.nchunks; ++j) {
       if (j < t.nchunks) {
         const uint32_t c = chunk + j;
         const uint32_t item = 2 * c, slot = item % L::NSLOT, use = item / L::NSLOT;
+        FGA_TS(p, it, j, 8);
         mbar_wait(&bar.kv_full[slot], use & 1);
+        FGA_TS(p, it, j, 9);
         fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
         tc_fence_after();
-        const uint32_t kaddr = smem_kv + slot * L::KV;
+        FGA_TS(p, it, j, 13);
+        const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
         const uint32_t tS = tmem + (c & 1) * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
-          umma_ss(tS, sdesc_sw128(qaddr + off, 16, 1024), sdesc_sw128(kaddr + off, 16, 1024), IDESC_S, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
+            umma_ss(tS, dq + off, dk + off, IDESC_S, kk > 0);
+          }
+          umma_commit(&bar.s_full[c & 1]);
+          umma_commit(&bar.kv_empty[slot]);
         }
-        umma_commit(&bar.s_full[c & 1]);
-        umma_commit(&bar.kv_empty[slot]);
+        __syncwarp();
+        FGA_TS(p, it, j, 14);
       }
       if (j >= 1) {
         const uint32_t c = chunk + j - 1;
+        FGA_TS(p, it, j - 1, 10);
         mbar_wait(&bar.p_full[c & 1], (c >> 1) & 1);
+        FGA_TS(p, it, j - 1, 11);
         const uint32_t item = 2 * c + 1, slot = item % L::NSLOT, use = item / L::NSLOT;
         mbar_wait(&bar.kv_full[slot], use & 1);
         fence_proxy_async_smem();
         tc_fence_after();
-        const uint32_t vaddr = smem_kv + slot * L::KV;
+        const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
         const uint32_t tP = tmem + (c & 1) * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
-          umma_ts(tO, tP + kk * 8, sdesc_sw128(vaddr + kk * 16 * 128, HALF, 1024), IDESC_O, (j > 1 || kk > 0) ? 1u : 0u);
-        umma_commit(&bar.kv_empty[slot]);
-        umma_commit(bar.pv_done);
+          for (int kk = 0; kk < BN / 16; ++kk)
+            umma_ts(tO, tP + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, (j > 1 || kk > 0) ? 1u : 0u);
+          umma_commit(&bar.kv_empty[slot]);
+          umma_commit(bar.pv_done);
+        }
+        __syncwarp();
+        FGA_TS(p, it, j - 1, 12);
       }
     }
-    umma_commit(&bar.o_full[ob]);
-    umma_commit(&bar.q_empty[qs]);
+    if (elect_one()) {
+      umma_commit(&bar.o_full[ob]);
+      umma_commit(&bar.q_empty[qs]);
+    }
+    __syncwarp();
     chunk += t.nchunks;
   }
 }
@@ -287,12 +313,15 @@ __device__ __forceinline__ void softmax_wg(const AttnParams& p, const Bars& bar,
     for (int j = 0; j < t.nchunks; ++j) {
       const uint32_t c = chunk + j;
       const uint32_t tS = tmem + (c & 1) * 128 + lane_off;
+      if (tid == 0) FGA_TS(p, it, j, 0);
       mbar_wait(&bar.s_full[c & 1], (c >> 1) & 1);
+      if (tid == 0) FGA_TS(p, it, j, 1);
       tc_fence_after();
       uint32_t s[4][32];
 #pragma unroll
       for (int q = 0; q < 4; ++q) tmem_ld32(tS + q * 32, s[q]);
       tmem_ld_wait();
+      if (tid == 0) FGA_TS(p, it, j, 2);
       const int nvalid = min(BN, t.count - j * BN);
       if (nvalid < BN) {
 #pragma unroll
@@ -306,6 +335,7 @@ __device__ __forceinline__ void softmax_wg(const AttnParams& p, const Bars& bar,
 #pragma unroll
       for (int i = 8; i < BN; ++i) mx[i & 7] = fmaxf(mx[i & 7], __uint_as_float(s[i >> 5][i & 31]));
       const float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+      if (tid == 0) FGA_TS(p, it, j, 3);
       float alpha = 1.f;
       bool rescale = false;
       if (j == 0) {
@@ -322,13 +352,17 @@ __device__ __forceinline__ void softmax_wg(const AttnParams& p, const Bars& bar,
       uint32_t pk[2][32];
 #pragma unroll
       for (int i = 0; i < BN / 2; ++i) {
-        const float p0 = ex2(fmaf(__uint_as_float(s[(2 * i) >> 5][(2 * i) & 31]), sl2, neg_m));
-        const float p1 = ex2(fmaf(__uint_as_float(s[(2 * i + 1) >> 5][(2 * i + 1) & 31]), sl2, neg_m));
+        const float x0 = fmaf(__uint_as_float(s[(2 * i) >> 5][(2 * i) & 31]), sl2, neg_m);
+        const float x1 = fmaf(__uint_as_float(s[(2 * i + 1) >> 5][(2 * i + 1) & 31]), sl2, neg_m);
+        const bool emu = (i % EMU_EVERY) == EMU_EVERY - 1;  // optional FMA-pipe exp2 share (off by default)
+        const float p0 = emu ? ex2_poly(x0) : ex2(x0);
+        const float p1 = emu ? ex2_poly(x1) : ex2(x1);
         sum[(2 * i) & 7] += p0;
         sum[(2 * i + 1) & 7] += p1;
         pk[i >> 5][i & 31] = pack_bf16(p0, p1);
       }
       const float rsum = ((sum[0] + sum[1]) + (sum[2] + sum[3])) + ((sum[4] + sum[5]) + (sum[6] + sum[7]));
+      if (tid == 0) FGA_TS(p, it, j, 4);
       l_run = l_run * alpha + rsum;
       tmem_st32(tS, pk[0]);
       tmem_st32(tS + 32, pk[1]);
@@ -350,6 +384,7 @@ __device__ __forceinline__ void softmax_wg(const AttnParams& p, const Bars& bar,
       tc_fence_before();
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(&bar.p_full[c & 1]);
+      if (tid == 0) FGA_TS(p, it, j, 5);
     }
     // ---- epilogue: O / l -> global  (tiled.py:73-77)
     mbar_wait(&bar.o_full[ob], (it >> 1) & 1);
@@ -378,13 +413,14 @@ __device__ __forceinline__ void softmax_wg(const AttnParams& p, const Bars& bar,
 }
 
 template <int D, bool OUT_F32, int NP, int G4>
-__global__ void __launch_bounds__(32 * (5 + NP), 1)
+__global__ void __launch_bounds__(32 * (NSOFT + 1 + NP), 1)
     fga_attn_ws_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmK2,
                        const __grid_constant__ CUtensorMap tmV2, const AttnParams p) {
   using L = WsSmem<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_ws[];
+  uint8_t* smem = smem_ws;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 atoms need 1 KB alignment
   const Bars bar = carve_bars<D>(smem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -395,9 +431,9 @@ __global__ void __launch_bounds__(32 * (5 + NP), 1)
       mbar_init(&bar.q_full[i], 1);
       mbar_init(&bar.q_empty[i], 1);
       mbar_init(&bar.s_full[i], 1);
-      mbar_init(&bar.p_full[i], 4);
+      mbar_init(&bar.p_full[i], NSOFT);
       mbar_init(&bar.o_full[i], 1);
-      mbar_init(&bar.o_empty[i], 4);
+      mbar_init(&bar.o_empty[i], NSOFT);
     }
     for (int i = 0; i < L::NSLOT; ++i) {
       mbar_init(&bar.kv_full[i], NP * 32 + 1);
@@ -415,14 +451,19 @@ __global__ void __launch_bounds__(32 * (5 + NP), 1)
   tc_fence_after();
   const uint32_t tmem = *bar.tmem_slot;
 
-  static_assert((5 + NP) % 4 == 0, "whole warpgroups are needed for setmaxnreg");
-  if (warp < 4) {
+  static_assert((NSOFT + 1 + NP) % 4 == 0, "whole warpgroups are needed for setmaxnreg");
+  // setmaxnreg.inc can only take registers this CTA released with .dec (its pool is threads x launch regs)
+  constexpr int kThreads = 32 * (NSOFT + 1 + NP);
+  constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8 > 255 ? 248 : (65536 / kThreads) / 8 * 8;
+  static_assert(32 * NSOFT * (REG_SOFTMAX - kLaunchRegs) <= (kThreads - 32 * NSOFT) * (kLaunchRegs - REG_OTHER),
+                "setmaxnreg budget would deadlock");
+  if (warp < NSOFT) {
     setmaxnreg_inc<REG_SOFTMAX>();
     softmax_wg<D, OUT_F32>(p, bar, tmem, tid);
   } else {
     setmaxnreg_dec<REG_OTHER>();
     if (warp == WARP_MMA) {
-      if (lane == 0) mma_issuer<D>(p, smem, bar, tmem);
+      mma_issuer<D>(p, smem, bar, tmem);
     } else {
       producer<D, NP, G4>(p, &tmQ, &tmK, &tmV, &tmK2, &tmV2, smem, bar, warp - WARP_PROD0, lane);
     }
@@ -435,8 +476,14 @@ __global__ void __launch_bounds__(32 * (5 + NP), 1)
   }
 }
 
-constexpr int NPROD = 15;  // producer warps (5 + NPROD must be a multiple of 4)
-constexpr int G4ROWS = 0;  // rows per K/V item gathered by TMA gather4 (rest by cp.async)
+#ifndef FGA_NPROD
+#define FGA_NPROD 15
+#endif
+#ifndef FGA_G4ROWS
+#define FGA_G4ROWS 0
+#endif
+constexpr int NPROD = FGA_NPROD;    // producer warps (NSOFT + 1 + NPROD must be a multiple of 4)
+constexpr int G4ROWS = FGA_G4ROWS;  // rows per K/V item gathered by TMA gather4 (rest by cp.async)
 
 template <int D, bool F32>
 int launch_ws(const CUtensorMap* maps, const AttnParams& p, cudaStream_t stream) {
@@ -449,7 +496,7 @@ int launch_ws(const CUtensorMap* maps, const AttnParams& p, cudaStream_t stream)
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t span = p.n_tiles - p.tile_begin;
   const int64_t grid = span < sms ? span : sms;
-  kern<<<static_cast<unsigned>(grid), 32 * (5 + NPROD), smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
+  kern<<<static_cast<unsigned>(grid), 32 * (NSOFT + 1 + NPROD), smem, stream>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
   return check_launch("fga_attn_ws_kernel");
 }
 
