@@ -72,6 +72,17 @@ int fga_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t 
                 int64_t idx_stride, int32_t* counts, int fill_sentinel, void* stream);
 
 /*
+ * Bit-packed slice masks: bit b of word w of a row is key 32w+b (8x fewer
+ * bytes than uint8 keep, e.g. for shipping masks from the host).
+ *   fga_pack_bits    : keep uint8 [rows, n] -> bits uint32 [rows, ceil(n/32)].
+ *   fga_compact_bits : same output contract as fga_compact without the
+ *                      argmax fallback (an empty row keeps count 0).
+ */
+int fga_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bits, void* stream);
+int fga_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx, int64_t idx_stride, int32_t* counts,
+                     int fill_sentinel, void* stream);
+
+/*
  * FG-Attn forward (K2 gather producer + K3 tcgen05 consumer).
  * Replaces sparse.py:111-156 (sparse_attention), whose numerics are the
  * online softmax of tiled.py:48-77; equals oracle.py:55-82

@@ -15,8 +15,9 @@ from .core import (GATHER, PRECISIONS, STREAM, AttnConfig, AttnMap, AttnTensor, 
                    TileEvent, analysis_scores, ingest, make_rng, new_tensor, round_bf16)
 from .masks import (STRATEGIES, CachedMaskState, MaskBuilderConfig, build_mask, build_mask_avg_query,
                     build_mask_cached, build_mask_cached_qk, cached_group_max, pooled_query_scores, refresh_policy)
+from .pipeline import pack_keep_bits, sparse_attention_host
 from .perfmodel import CostReport, count_flops, flop_speedup, synthetic_trace, trace_flops
-from .sparse import (DeviceIndexMask, PackedTile, SparseIndexMask, compact_keep, export_padded, full_mask,
+from .sparse import (DeviceIndexMask, PackedTile, SparseIndexMask, compact_keep, compact_keep_bits, export_padded, full_mask,
                      gather_rows, import_padded, mask_density, mask_jaccard, masked_dense_attention, random_mask,
                      random_mask_device, sparse_attention)
 from .tiled import dense_attention, flash_attention

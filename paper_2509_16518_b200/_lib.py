@@ -34,6 +34,8 @@ _SIGS = {
     "fga_last_error": ([], ctypes.c_char_p),
     "fga_device_supported": ([_I], _I),
     "fga_compact": ([_P, _P, _I64, _I64, _P, _I64, _P, _I, _P], _I),
+    "fga_pack_bits": ([_P, _I64, _I64, _P, _P], _I),
+    "fga_compact_bits": ([_P, _I64, _I64, _P, _I64, _P, _I, _P], _I),
     "fga_sparse_attn_fwd": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _P], _I),
     "fga_sparse_attn_fwd_tiles": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _I64, _I64, _P], _I),
     "fga_dense_attn_fwd": ([_P, _P, _P, _P, _I, _P, FgaShape, _P], _I),

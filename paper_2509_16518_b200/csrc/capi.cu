@@ -98,6 +98,17 @@ int fga_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t 
                         static_cast<cudaStream_t>(stream));
 }
 
+int fga_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bits, void* stream) {
+  if (rows > 0 && (!keep || !bits)) return fail(FGA_EINVAL, "null pointer");
+  return launch_pack_bits(keep, rows, n, bits, static_cast<cudaStream_t>(stream));
+}
+
+int fga_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx, int64_t idx_stride, int32_t* counts,
+                     int fill_sentinel, void* stream) {
+  if (rows > 0 && (!bits || !idx || !counts)) return fail(FGA_EINVAL, "null pointer");
+  return launch_compact_bits(bits, rows, n, idx, idx_stride, counts, fill_sentinel, static_cast<cudaStream_t>(stream));
+}
+
 int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
                         const int32_t* counts, void* o, int o_dtype, float* lse, fga_shape shape, void* stream) {
   int rc = check_shape(shape);

@@ -4,11 +4,15 @@
 //                                                        empty -> [argmax(scores)])
 //   /root/reference/pkg/src/sliceattn/sparse.py:165-175 (export_padded: -1 tail)
 //
+// Two input formats: uint8 keep bytes (fga_compact) and bit-packed keep words
+// (fga_compact_bits, 8x fewer bytes to read or to ship from the host).
+//
 // One CTA per (b,h,g) row.  Each thread reads one aligned 16-byte block of
 // keep bytes per round, turns it into a 16-bit occupancy mask, and a
 // warp-shuffle + shared-memory block scan of the popcounts gives every
-// thread its output offset, so positions are written in ascending order
-// without any sort.  HBM-bound: read n bytes, write 4*count (+4*(n-count)).
+// thread its offset in a shared-memory stage, so positions come out in
+// ascending order without any sort and leave the CTA as coalesced stores.
+// HBM-bound: read n bytes (n/8 for bits), write 4*count (+4*(n-count)).
 #include "internal.h"
 
 namespace fga {
@@ -32,6 +36,7 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
   __shared__ int s_total;
   __shared__ float s_bv[W];
   __shared__ int s_bi[W];
+  __shared__ int s_stage[T * 16];  // one round's positions, written out coalesced
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint8_t* kr = keep + row * n;
@@ -79,14 +84,16 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
       if (lane == W - 1) s_total = sc;
     }
     __syncthreads();
-    int off = running + s_warp[warp] + incl - cnt;
+    int off = s_warp[warp] + incl - cnt;
     const int key0 = static_cast<int>(blk * 16 - head);
     while (bits) {
-      const int b = __ffs(bits) - 1;
-      out[off++] = key0 + b;
+      s_stage[off++] = key0 + __ffs(bits) - 1;
       bits &= bits - 1;
     }
-    running += s_total;
+    __syncthreads();
+    const int total = s_total;
+    for (int i = tid; i < total; i += T) out[running + i] = s_stage[i];
+    running += total;
     __syncthreads();
   }
 
@@ -119,7 +126,112 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
     for (int64_t i = running + tid; i < n; i += T) out[i] = -1;
 }
 
+// ---------------------------------------------------------------- bit-packed masks
+// keep bits: uint32 words, bit b of word w = key 32w + b.  Packing (one warp
+// ballot per 32 keys) and compaction from bits: each thread scans WPT words
+// per round, so a CTA covers 256 * WPT * 32 keys per round with one block scan.
+__global__ void __launch_bounds__(256) fga_pack_bits_kernel(const uint8_t* __restrict__ keep, int64_t rows, int64_t n,
+                                                             int64_t words, uint32_t* __restrict__ bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t wi = warp; wi < rows * words; wi += nwarps) {
+    const int64_t row = wi / words, w = wi % words;
+    const int64_t key = w * 32 + lane;
+    const bool on = key < n && keep[row * n + key] != 0;
+    const uint32_t b = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) bits[wi] = b;
+  }
+}
+
+constexpr int WPT = 1;
+
+__global__ void __launch_bounds__(T) fga_compact_bits_kernel(const uint32_t* __restrict__ bits, int64_t words,
+                                                             int64_t n, int32_t* __restrict__ idx, int64_t stride,
+                                                             int32_t* __restrict__ counts, int fill) {
+  __shared__ int s_warp[W];
+  __shared__ int s_total;
+  __shared__ int s_stage[T * WPT * 32];
+  const int64_t row = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t* br = bits + row * words;
+  int32_t* out = idx + row * stride;
+  int running = 0;
+  for (int64_t w0 = 0; w0 < words; w0 += int64_t(T) * WPT) {
+    uint32_t m[WPT];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < WPT; ++u) {
+      const int64_t w = w0 + int64_t(tid) * WPT + u;
+      uint32_t v = w < words ? __ldg(br + w) : 0u;
+      const int64_t k0 = w * 32;
+      if (k0 + 32 > n) v &= (k0 >= n) ? 0u : ((1u << (n - k0)) - 1u);  // keys past n are not keys
+      m[u] = v;
+      cnt += __popc(v);
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int v = lane < W ? s_warp[lane] : 0;
+      int sc = v;
+#pragma unroll
+      for (int o = 1; o < W; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, sc, o);
+        if (lane >= o) sc += t;
+      }
+      if (lane < W) s_warp[lane] = sc - v;
+      if (lane == W - 1) s_total = sc;
+    }
+    __syncthreads();
+    int off = s_warp[warp] + incl - cnt;
+#pragma unroll
+    for (int u = 0; u < WPT; ++u) {
+      uint32_t v = m[u];
+      const int key0 = static_cast<int>((w0 + int64_t(tid) * WPT + u) * 32);
+      while (v) {
+        s_stage[off++] = key0 + __ffs(v) - 1;
+        v &= v - 1;
+      }
+    }
+    __syncthreads();
+    const int total = s_total;
+    for (int i = tid; i < total; i += T) out[running + i] = s_stage[i];
+    running += total;
+    __syncthreads();
+  }
+  if (tid == 0) counts[row] = running;
+  if (fill)
+    for (int64_t i = running + tid; i < n; i += T) out[i] = -1;
+}
+
 }  // namespace
+
+int launch_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bits, cudaStream_t stream) {
+  if (rows < 0 || n <= 0) return fail(FGA_EINVAL, "pack_bits: need rows >= 0, n > 0");
+  if (rows == 0) return FGA_OK;
+  const int64_t words = (n + 31) / 32;
+  const int64_t warps = rows * words;
+  const int64_t blocks = (warps + 7) / 8 < 148 * 16 ? (warps + 7) / 8 : 148 * 16;
+  fga_pack_bits_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(keep, rows, n, words, bits);
+  return check_launch("fga_pack_bits_kernel");
+}
+
+int launch_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx, int64_t idx_stride,
+                        int32_t* counts, int fill, cudaStream_t stream) {
+  if (rows < 0 || n <= 0 || idx_stride < n) return fail(FGA_EINVAL, "compact_bits: need rows >= 0, n > 0, idx_stride >= n");
+  if (n >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact_bits: n must be < 2^31");
+  if (rows == 0) return FGA_OK;
+  if (rows >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact_bits: too many rows");
+  fga_compact_bits_kernel<<<static_cast<unsigned>(rows), T, 0, stream>>>(bits, (n + 31) / 32, n, idx, idx_stride,
+                                                                           counts, fill);
+  return check_launch("fga_compact_bits_kernel");
+}
 
 int launch_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t n, int32_t* idx,
                    int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream) {

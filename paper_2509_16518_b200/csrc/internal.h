@@ -27,6 +27,9 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
                 cudaStream_t stream, int64_t tile_begin = 0, int64_t tile_end = -1);
 int launch_gather(const void* matrix, int64_t rows, int64_t d, const int32_t* indices, int64_t n_idx, void* out,
                   cudaStream_t stream);
+int launch_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bits, cudaStream_t stream);
+int launch_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx, int64_t idx_stride,
+                        int32_t* counts, int fill, cudaStream_t stream);
 int launch_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t n, int32_t* idx,
                    int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream);
 

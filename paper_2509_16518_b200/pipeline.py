@@ -1,0 +1,120 @@
+"""Host-resident inputs: overlap PCIe transfers with the kernels.
+
+``sparse_attention_host(q, k, v, keep_bits, cfg)`` takes pinned CPU tensors
+(bf16 Q/K/V [B,H,N,D], uint32 bit-packed slice mask [B,H,G,ceil(N/32)]) and
+fills a pinned CPU output.  The (b,h) heads are cut into slabs; slab s+1's
+H2D copy (copy engine), slab s's K1b bit compaction + attention (SMs) and
+slab s-1's D2H copy run concurrently on three streams, so the step costs
+about max(H2D, compute, D2H) instead of their sum.  Heads are independent
+(sparse.py:138-155), so slabs need no exchange.  The call is stream-ordered
+after the caller's current stream and makes that stream wait for the last
+D2H, so CUDA events on the caller's stream time the whole transfer+compute.
+"""
+
+from __future__ import annotations
+
+from . import _lib
+from ._device import ptr, require_device, torch
+from .core import AttnConfig, ShapeError
+
+__all__ = ["pack_keep_bits", "HostPipeline", "sparse_attention_host"]
+
+
+def pack_keep_bits(keep):
+    """uint8/bool keep [..., N] (CUDA) -> uint32 bits [..., ceil(N/32)] (fga_pack_bits)."""
+    t = torch()
+    require_device()
+    keep = keep.to(t.uint8).contiguous()
+    n = keep.shape[-1]
+    rows = keep.numel() // n
+    words = (n + 31) // 32
+    bits = t.empty(tuple(keep.shape[:-1]) + (words,), dtype=t.int32, device=keep.device)
+    _lib.call("fga_pack_bits", ptr(keep), rows, n, ptr(bits), t.cuda.current_stream().cuda_stream)
+    return bits
+
+
+class HostPipeline:
+    """Device buffers + streams for one problem shape (reused across calls)."""
+
+    def __init__(self, cfg: AttnConfig, slabs: int = 4, device=None):
+        t = torch()
+        self.dev = require_device(device)
+        self.cfg = cfg
+        bh = cfg.batch * cfg.heads
+        slabs = max(1, min(slabs, bh))
+        base, extra = divmod(bh, slabs)
+        self.ranges, h0 = [], 0
+        for s in range(slabs):
+            h1 = h0 + base + (1 if s < extra else 0)
+            self.ranges.append((h0, h1))
+            h0 = h1
+        n, d, g = cfg.seq_len, cfg.head_dim, cfg.num_groups
+        self.words = (n + 31) // 32
+        kw = dict(device=f"cuda:{self.dev}")
+        self.q = t.empty((bh, n, d), dtype=t.bfloat16, **kw)
+        self.k = t.empty_like(self.q)
+        self.v = t.empty_like(self.q)
+        self.o = t.empty_like(self.q)
+        self.bits = t.empty((bh, g, self.words), dtype=t.int32, **kw)
+        self.idx = t.empty((bh, g, n), dtype=t.int32, **kw)
+        self.counts = t.empty((bh, g), dtype=t.int32, **kw)
+        self.s_h2d = t.cuda.Stream(self.dev)
+        self.s_cmp = t.cuda.Stream(self.dev)
+        self.s_d2h = t.cuda.Stream(self.dev)
+
+    def __call__(self, q, k, v, keep_bits, out):
+        t = torch()
+        cfg = self.cfg
+        bh, n, d, g = cfg.batch * cfg.heads, cfg.seq_len, cfg.head_dim, cfg.num_groups
+        hq, hk, hv, ho = (x.view(bh, n, d) for x in (q, k, v, out))
+        hb = keep_bits.view(bh, g, self.words)
+        caller = t.cuda.current_stream(self.dev)
+        start = caller.record_event()
+        for s_ in (self.s_h2d, self.s_cmp, self.s_d2h):
+            s_.wait_event(start)
+        last = None
+        for h0, h1 in self.ranges:
+            with t.cuda.stream(self.s_h2d):
+                for dst, src in ((self.bits, hb), (self.q, hq), (self.k, hk), (self.v, hv)):
+                    dst[h0:h1].copy_(src[h0:h1], non_blocking=True)
+                ev_in = self.s_h2d.record_event()
+            self.s_cmp.wait_event(ev_in)
+            rows = (h1 - h0) * g
+            sh = _lib.shape(1, h1 - h0, n, d, cfg.group_size, cfg.scale)
+            cs = self.s_cmp.cuda_stream
+            _lib.call("fga_compact_bits", ptr(self.bits[h0]), rows, n, ptr(self.idx[h0]), n, ptr(self.counts[h0]), 0, cs)
+            _lib.call("fga_sparse_attn_fwd", ptr(self.q[h0]), ptr(self.k[h0]), ptr(self.v[h0]), ptr(self.idx[h0]), n,
+                      ptr(self.counts[h0]), ptr(self.o[h0]), _lib.FGA_OUT_BF16, None, sh, cs)
+            ev_c = self.s_cmp.record_event()
+            self.s_d2h.wait_event(ev_c)
+            with t.cuda.stream(self.s_d2h):
+                ho[h0:h1].copy_(self.o[h0:h1], non_blocking=True)
+                last = self.s_d2h.record_event()
+        caller.wait_event(last)
+        # keep the host buffers alive until the copies complete (stream-ordered on `caller`)
+        for x in (q, k, v, keep_bits, out):
+            x.record_stream(caller) if x.is_cuda else None
+        return out
+
+
+_pipes: dict = {}
+
+
+def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: int = 4):
+    """FG-Attn from pinned host buffers (see module doc).  Returns the pinned host output;
+    synchronise the current stream before reading it."""
+    t = torch()
+    for x in (q, k, v):
+        if tuple(x.shape) != cfg.dims:
+            raise ShapeError(f"tensor dims {tuple(x.shape)} do not match config {cfg.dims}")
+        if x.dtype != t.bfloat16 or x.is_cuda:
+            raise ShapeError("q, k, v must be host bf16 tensors (pinned for overlap)")
+    expect = (cfg.batch, cfg.heads, cfg.num_groups, (cfg.seq_len + 31) // 32)
+    if tuple(keep_bits.shape) != expect:
+        raise ShapeError(f"keep_bits must be {expect}, got {tuple(keep_bits.shape)}")
+    key = (cfg, slabs, require_device())
+    if key not in _pipes:
+        _pipes[key] = HostPipeline(cfg, slabs)
+    if out is None:
+        out = t.empty(cfg.dims, dtype=t.bfloat16, pin_memory=True)
+    return _pipes[key](q, k, v, keep_bits, out)

@@ -33,7 +33,7 @@ from .core import GATHER, AttnConfig, AttnTensor, NumericError, ShapeError, Tile
 __all__ = [
     "SparseIndexMask", "DeviceIndexMask", "PackedTile", "gather_rows", "sparse_attention",
     "masked_dense_attention", "mask_density", "export_padded", "import_padded", "full_mask", "random_mask",
-    "random_mask_device", "compact_keep", "mask_jaccard", "chunk_trace",
+    "random_mask_device", "compact_keep", "compact_keep_bits", "mask_jaccard", "chunk_trace",
 ]
 
 
@@ -230,6 +230,24 @@ def compact_keep(keep, group_size: int, scores=None, fill_sentinel: bool = False
     cnt = t.empty((b, h, g), dtype=t.int32, device=keep.device)
     _lib.call("fga_compact", ptr(keep), ptr(sc), b * h * g, n, ptr(idx), n, ptr(cnt), int(fill_sentinel), stream_ptr())
     return DeviceIndexMask(b, h, n, group_size, idx, cnt)
+
+
+def compact_keep_bits(bits, group_size: int, seq_len: int, fill_sentinel: bool = False) -> DeviceIndexMask:
+    """Bit-packed keep words [B, H, G, ceil(N/32)] (int32/uint32, CUDA) -> DeviceIndexMask
+    (fga_compact_bits).  Same positions as compact_keep; no argmax fallback."""
+    t = torch()
+    require_device()
+    bits = as_device(bits, t.int32)
+    if bits.dim() != 4 or bits.shape[-1] != (seq_len + 31) // 32:
+        raise ShapeError("bits must be [B, H, G, ceil(N/32)]")
+    b, h, g, _ = bits.shape
+    if g != -(-seq_len // group_size):
+        raise ShapeError(f"bits have {g} groups, group_size {group_size} implies {-(-seq_len // group_size)}")
+    idx = t.empty((b, h, g, seq_len), dtype=t.int32, device=bits.device)
+    cnt = t.empty((b, h, g), dtype=t.int32, device=bits.device)
+    _lib.call("fga_compact_bits", ptr(bits), b * h * g, seq_len, ptr(idx), seq_len, ptr(cnt), int(fill_sentinel),
+              stream_ptr())
+    return DeviceIndexMask(b, h, seq_len, group_size, idx, cnt)
 
 
 # ---------------------------------------------------------------- K2 gather

@@ -168,3 +168,28 @@ def test_sharded_tile_ranges_reassemble_bitwise():
         shard.sparse_attention_shard(q, k, v, dm, cfg, rng_, out)
     torch.cuda.synchronize()
     assert torch.equal(out, full)
+
+
+def test_bit_packed_compaction_matches_bytes():
+    rng = np.random.default_rng(7)
+    for n in (1000, 4096, 33):
+        g = -(-n // 16)
+        keep = torch.from_numpy((rng.random((1, 2, g, n)) < 0.37).astype(np.uint8)).cuda()
+        bits = fga.pack_keep_bits(keep)
+        assert bits.shape == (1, 2, g, (n + 31) // 32)
+        a = fga.compact_keep(keep, 16, fill_sentinel=True)
+        b = fga.compact_keep_bits(bits, 16, n, fill_sentinel=True)
+        assert torch.equal(a.idx, b.idx) and torch.equal(a.counts, b.counts)
+
+
+def test_host_pipeline_equals_device_path():
+    cfg = fga.AttnConfig(1, 5, 2048, 128)
+    q, k, v = (torch.randn(cfg.dims, device="cuda").to(torch.bfloat16) for _ in range(3))
+    keep = (torch.rand((1, 5, cfg.num_groups, cfg.seq_len), device="cuda") < 0.3).to(torch.uint8)
+    ref = fga.sparse_attention(q, k, v, fga.compact_keep(keep, 128), cfg)
+    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+    hb = fga.pack_keep_bits(keep).cpu().pin_memory()
+    for slabs in (1, 2, 4):
+        out = fga.sparse_attention_host(hq, hk, hv, hb, cfg, slabs=slabs)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref.cpu()), slabs
