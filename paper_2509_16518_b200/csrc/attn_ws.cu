@@ -38,11 +38,15 @@
 namespace fga {
 namespace {
 
-constexpr int NSOFT = 4;  // softmax warps (one warpgroup: thread t owns row t)
+#ifndef FGA_PINGPONG
+#define FGA_PINGPONG 1
+#endif
+// softmax warps: ping-pong = two warpgroups on alternate chunks, else one warpgroup
+constexpr int NSOFT = FGA_PINGPONG ? 8 : 4;
 constexpr int WARP_MMA = NSOFT;
 constexpr int WARP_PROD0 = NSOFT + 1;
-constexpr int REG_SOFTMAX = 232;
-constexpr int REG_OTHER = 48;
+constexpr int REG_SOFTMAX = FGA_PINGPONG ? 176 : 232;
+constexpr int REG_OTHER = FGA_PINGPONG ? 40 : 48;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units (factor 256)
 #ifndef FGA_EMU_EVERY
 #define FGA_EMU_EVERY (1 << 20)
@@ -56,8 +60,9 @@ struct WsSmem {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_KV = OFF_Q + 2 * KV;
   static constexpr int OFF_BAR = OFF_KV + NSLOT * KV;
-  static constexpr int NBAR = 2 + 2 + 2 * NSLOT + 2 + 2 + 1 + 2 + 2;
-  static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
+  static constexpr int NBAR = 2 + 2 + 2 * NSLOT + 2 + 2 + 2 + 2 + 2;
+  static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // ping-pong merge: 2 WG x (m, l) x 128
+  static constexpr int BYTES = OFF_XCH + (FGA_PINGPONG ? 2 * 2 * 128 * 4 : 0);
   static constexpr int ALLOC = BYTES;  // extern smem is declared __align__(1024)
 };
 
@@ -68,7 +73,7 @@ struct Bars {
   uint64_t* kv_empty;  // [NSLOT]
   uint64_t* s_full;    // [2]
   uint64_t* p_full;    // [2]
-  uint64_t* pv_done;   // [1]
+  uint64_t* pv_done;   // [2] (ping-pong: one per O accumulator)
   uint64_t* o_full;    // [2]
   uint64_t* o_empty;   // [2]
   uint32_t* tmem_slot;
@@ -86,7 +91,7 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   r.s_full = b + 4 + 2 * L::NSLOT;
   r.p_full = r.s_full + 2;
   r.pv_done = r.p_full + 2;
-  r.o_full = r.pv_done + 1;
+  r.o_full = r.pv_done + 2;
   r.o_empty = r.o_full + 2;
   r.tmem_slot = reinterpret_cast<uint32_t*>(r.o_empty + 2);
   return r;
@@ -236,9 +241,8 @@ __device__ __forceinline__ void mma_issuer(const AttnParams& p, uint8_t* smem, c
   for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
     const int qs = it & 1, ob = it & 1;
-    const uint32_t tO = tmem + 256 + ob * 128;
     mbar_wait(&bar.q_full[qs], (it >> 1) & 1);
-    mbar_wait(&bar.o_empty[ob], ((it >> 1) & 1) ^ 1);
+    if (!FGA_PINGPONG) mbar_wait(&bar.o_empty[ob], ((it >> 1) & 1) ^ 1);
     tc_fence_after();
     const uint64_t dq = dq0 + ((qs * L::KV) >> 4);
     for (int j = 0; j <= t.nchunks; ++j) {
@@ -267,6 +271,13 @@ __device__ __forceinline__ void mma_issuer(const AttnParams& p, uint8_t* smem, c
       }
       if (j >= 1) {
         const uint32_t c = chunk + j - 1;
+        // ping-pong: O[c&1] per softmax warpgroup, one O set per tile (freed by the merged epilogue)
+        const uint32_t tO = tmem + 256 + (FGA_PINGPONG ? (c & 1) : ob) * 128;
+        const bool first_pv = FGA_PINGPONG ? (j - 1 < 2) : (j == 1);
+        if (FGA_PINGPONG && j == 1) {
+          mbar_wait(&bar.o_empty[0], (it & 1) ^ 1);
+          tc_fence_after();
+        }
         FGA_TS(p, it, j - 1, 10);
         mbar_wait(&bar.p_full[c & 1], (c >> 1) & 1);
         FGA_TS(p, it, j - 1, 11);
@@ -279,16 +290,16 @@ __device__ __forceinline__ void mma_issuer(const AttnParams& p, uint8_t* smem, c
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
-            umma_ts(tO, tP + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, (j > 1 || kk > 0) ? 1u : 0u);
+            umma_ts(tO, tP + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, (!first_pv || kk > 0) ? 1u : 0u);
           umma_commit(&bar.kv_empty[slot]);
-          umma_commit(bar.pv_done);
+          umma_commit(&bar.pv_done[FGA_PINGPONG ? (c & 1) : 0]);
         }
         __syncwarp();
         FGA_TS(p, it, j - 1, 12);
       }
     }
     if (elect_one()) {
-      umma_commit(&bar.o_full[ob]);
+      umma_commit(&bar.o_full[FGA_PINGPONG ? 0 : ob]);
       umma_commit(&bar.q_empty[qs]);
     }
     __syncwarp();
@@ -368,7 +379,7 @@ __device__ __forceinline__ void softmax_wg(const AttnParams& p, const Bars& bar,
       tmem_st32(tS + 32, pk[1]);
       if (__any_sync(0xffffffffu, rescale)) {
         // O holds PV_{c-1}: wait for it, then scale this warp's rows in place
-        mbar_wait(bar.pv_done, (c - 1) & 1);
+        mbar_wait(&bar.pv_done[0], (c - 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int q = 0; q < D / 32; ++q) {
@@ -412,6 +423,141 @@ __device__ __forceinline__ void softmax_wg(const AttnParams& p, const Bars& bar,
   }
 }
 
+// ------------------------------------------------------------------ ping-pong softmax (256 threads)
+// Warpgroup wg (warps 4wg..4wg+3) owns the chunks with c % 2 == wg: S/P buffer
+// S[wg], its own running max / sum and its own accumulator O[wg].  The two
+// groups are never lock-stepped, so one group's MUFU-heavy exp phase overlaps
+// the other's TMEM loads, max and stores (two softmax warps per SMSP).  The
+// epilogue merges (m, l, O) of both groups:
+//   O = (O0 2^(m0-M) + O1 2^(m1-M)) / (l0 2^(m0-M) + l1 2^(m1-M)),  M = max(m0, m1)
+// each group writing half of the output columns.  (A two-pass TMEM read to save
+// registers cost six load->wait round trips per chunk and ran 1.7x slower.)
+__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+template <int D, bool OUT_F32>
+__device__ __forceinline__ void softmax_pp(const AttnParams& p, const Bars& bar, uint32_t tmem, int tid, float* xch) {
+  const int warp = tid >> 5, wg = warp >> 2, row = tid & 127;
+  const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  const uint32_t tS = tmem + wg * 128 + lane_off;
+  const uint32_t tOw = tmem + 256 + wg * 128 + lane_off;
+  const float sl2 = p.scale_log2;
+  uint32_t chunk = 0;
+  int it = 0;
+  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+    const Tile t = decode_tile(p, tile);
+    float m_use = -INFINITY, l_run = 0.f;
+    const int j0 = (wg - static_cast<int>(chunk & 1)) & 1;
+    for (int j = j0; j < t.nchunks; j += 2) {
+      const uint32_t c = chunk + j;
+      if (row == 0 && wg == 0) FGA_TS(p, it, j, 0);
+      mbar_wait(&bar.s_full[wg], (c >> 1) & 1);
+      if (row == 0 && wg == 0) FGA_TS(p, it, j, 1);
+      tc_fence_after();
+      const int nvalid = min(BN, t.count - j * BN);
+      uint32_t sv[4][32];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_ld32(tS + q * 32, sv[q]);
+      tmem_ld_wait();
+      if (row == 0 && wg == 0) FGA_TS(p, it, j, 2);
+      if (nvalid < BN) {
+#pragma unroll
+        for (int i = 0; i < BN; ++i)
+          if (i >= nvalid) sv[i >> 5][i & 31] = __float_as_uint(-INFINITY);
+      }
+      float mx[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) mx[a] = __uint_as_float(sv[0][a]);
+#pragma unroll
+      for (int i = 8; i < BN; ++i) mx[i & 7] = fmaxf(mx[i & 7], __uint_as_float(sv[i >> 5][i & 31]));
+      const float rmax =
+          fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+      if (row == 0 && wg == 0) FGA_TS(p, it, j, 3);
+      float alpha = 1.f;
+      bool rescale = false;
+      if (j < 2) {  // this group's first chunk of the tile
+        m_use = rmax;
+      } else if (rmax - m_use > RESCALE_THRESHOLD) {
+        alpha = ex2(m_use - rmax);
+        m_use = rmax;
+        rescale = true;
+      }
+      const float neg_m = -m_use;
+      float sum[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) sum[a] = 0.f;
+      uint32_t pk[2][32];
+#pragma unroll
+      for (int i = 0; i < BN / 2; ++i) {
+        const float p0 = ex2(fmaf(__uint_as_float(sv[(2 * i) >> 5][(2 * i) & 31]), sl2, neg_m));
+        const float p1 = ex2(fmaf(__uint_as_float(sv[(2 * i + 1) >> 5][(2 * i + 1) & 31]), sl2, neg_m));
+        sum[(2 * i) & 7] += p0;
+        sum[(2 * i + 1) & 7] += p1;
+        pk[i >> 5][i & 31] = pack_bf16(p0, p1);
+      }
+      tmem_st32(tS, pk[0]);
+      tmem_st32(tS + 32, pk[1]);
+      const float rsum = ((sum[0] + sum[1]) + (sum[2] + sum[3])) + ((sum[4] + sum[5]) + (sum[6] + sum[7]));
+      if (row == 0 && wg == 0) FGA_TS(p, it, j, 4);
+      l_run = l_run * alpha + rsum;
+      if (__any_sync(0xffffffffu, rescale)) {
+        // O[wg] holds PV of this group's previous chunk (c - 2): wait for it, then scale in place
+        mbar_wait(&bar.pv_done[wg], ((c - 2) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int q = 0; q < D / 32; ++q) {
+          uint32_t o[32];
+          tmem_ld32(tOw + q * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(tOw + q * 32, o);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&bar.p_full[wg]);
+      if (row == 0 && wg == 0) FGA_TS(p, it, j, 5);
+    }
+    // ---- epilogue: merge the two groups' partial softmax, O / l -> global (tiled.py:73-77)
+    xch[(wg * 2) * 128 + row] = m_use;
+    xch[(wg * 2 + 1) * 128 + row] = l_run;
+    softmax_bar();
+    const float m0 = xch[row], l0 = xch[128 + row], m1 = xch[256 + row], l1 = xch[384 + row];
+    softmax_bar();  // both groups have read before the next tile rewrites xch
+    const float M = fmaxf(l0 > 0.f ? m0 : -INFINITY, l1 > 0.f ? m1 : -INFINITY);
+    const float s0 = l0 > 0.f ? ex2(m0 - M) : 0.f;
+    const float s1 = l1 > 0.f ? ex2(m1 - M) : 0.f;
+    const float L = l0 * s0 + l1 * s1;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    mbar_wait(&bar.o_full[0], it & 1);
+    tc_fence_after();
+    const bool valid = row < t.rows;
+    const int64_t out_row = static_cast<int64_t>(t.row0) + t.q0 + row;
+#pragma unroll
+    for (int q = 0; q < D / 64; ++q) {
+      const int col = wg * (D / 2) + q * 32;
+      uint32_t o0[32], o1[32];
+      tmem_ld32(tmem + 256 + lane_off + col, o0);
+      tmem_ld32(tmem + 384 + lane_off + col, o1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float a = s0 > 0.f ? __uint_as_float(o0[i]) * s0 : 0.f;  // an unused accumulator holds stale bits
+        const float b = s1 > 0.f ? __uint_as_float(o1[i]) * s1 : 0.f;
+        o0[i] = __float_as_uint(a + b);
+      }
+      if (valid) store_row32<OUT_F32>(p.out, out_row * D + col, o0, inv);
+    }
+    tc_fence_before();
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&bar.o_empty[0]);
+    if (wg == 0 && valid && p.lse != nullptr)
+      p.lse[out_row] = L > 0.f ? M * 0.69314718055994531f + logf(L) : -INFINITY;
+    chunk += t.nchunks;
+  }
+}
+
 template <int D, bool OUT_F32, int NP, int G4>
 __global__ void __launch_bounds__(32 * (NSOFT + 1 + NP), 1)
     fga_attn_ws_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -431,15 +577,16 @@ __global__ void __launch_bounds__(32 * (NSOFT + 1 + NP), 1)
       mbar_init(&bar.q_full[i], 1);
       mbar_init(&bar.q_empty[i], 1);
       mbar_init(&bar.s_full[i], 1);
-      mbar_init(&bar.p_full[i], NSOFT);
+      mbar_init(&bar.p_full[i], FGA_PINGPONG ? 4 : NSOFT);
       mbar_init(&bar.o_full[i], 1);
-      mbar_init(&bar.o_empty[i], NSOFT);
+      mbar_init(&bar.o_empty[i], NSOFT);  // every softmax warp arrives once per tile
     }
     for (int i = 0; i < L::NSLOT; ++i) {
       mbar_init(&bar.kv_full[i], NP * 32 + 1);
       mbar_init(&bar.kv_empty[i], 1);
     }
-    mbar_init(bar.pv_done, 1);
+    mbar_init(&bar.pv_done[0], 1);
+    mbar_init(&bar.pv_done[1], 1);
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -459,7 +606,10 @@ __global__ void __launch_bounds__(32 * (NSOFT + 1 + NP), 1)
                 "setmaxnreg budget would deadlock");
   if (warp < NSOFT) {
     setmaxnreg_inc<REG_SOFTMAX>();
-    softmax_wg<D, OUT_F32>(p, bar, tmem, tid);
+    if constexpr (FGA_PINGPONG)
+      softmax_pp<D, OUT_F32>(p, bar, tmem, tid, reinterpret_cast<float*>(smem + L::OFF_XCH));
+    else
+      softmax_wg<D, OUT_F32>(p, bar, tmem, tid);
   } else {
     setmaxnreg_dec<REG_OTHER>();
     if (warp == WARP_MMA) {
@@ -477,7 +627,7 @@ __global__ void __launch_bounds__(32 * (NSOFT + 1 + NP), 1)
 }
 
 #ifndef FGA_NPROD
-#define FGA_NPROD 15
+#define FGA_NPROD (FGA_PINGPONG ? 11 : 15)
 #endif
 #ifndef FGA_G4ROWS
 #define FGA_G4ROWS 0
