@@ -27,16 +27,32 @@ struct AttnParams {
   int heads, seq_len, group_size, groups, tiles_per_group;
   float scale_log2;
   int dense;
-  long long* trace;  // debug timeline (FGA_TRACE=<file>): CTA 0, first tile, clock64 per phase
+  long long* trace;  // debug timeline (FGA_TRACE=<file>): CTA 0, tile iteration trace_it, clock64 per phase
+  int trace_it;      // FGA_TRACE_IT (default 0)
 };
 
-// Debug timeline hook: slot s of chunk j (j < 64) for CTA 0's first tile.
+// Debug timeline hooks (FGA_TRACE=<file>).  Chunk level: slot s of chunk j
+// (j < 64) of CTA 0's tile iteration p.trace_it.  Tile level: slot s of CTA 0's
+// tile iteration it (< 32).  CTA level: %globaltimer at start / end of every CTA.
 #define FGA_TRACE_SLOTS 16
+#define FGA_TRACE_TILE_OFF (64 * FGA_TRACE_SLOTS)
+#define FGA_TRACE_CTA_OFF (FGA_TRACE_TILE_OFF + 32 * 8)
+#define FGA_TRACE_LEN (FGA_TRACE_CTA_OFF + 2 * 1024)
 #define FGA_TS(p, it, j, slot)                                                                         \
   do {                                                                                                  \
-    if ((p).trace != nullptr && blockIdx.x == 0 && (it) == 0 && (j) < 64)                               \
+    if ((p).trace != nullptr && blockIdx.x == 0 && (it) == (p).trace_it && (j) < 64)                    \
       (p).trace[(j) * FGA_TRACE_SLOTS + (slot)] = clock64();                                            \
   } while (0)
+#define FGA_TT(p, it, slot)                                                                            \
+  do {                                                                                                  \
+    if ((p).trace != nullptr && blockIdx.x == 0 && (it) < 32)                                           \
+      (p).trace[FGA_TRACE_TILE_OFF + (it) * 8 + (slot)] = clock64();                                    \
+  } while (0)
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // One work tile: <=128 query rows of group (b,h,g) and that group's key list.
 struct Tile {
@@ -85,7 +101,8 @@ __device__ __forceinline__ void store_row32(void* out, int64_t off, const uint32
   }
 }
 
-int launch_attn_ws(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
+int launch_attn_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, int d, bool out_f32,
+                   cudaStream_t stream);
 int launch_attn_sync(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
 
 }  // namespace fga

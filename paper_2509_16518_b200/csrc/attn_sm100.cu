@@ -318,14 +318,15 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
 
   const bool f32 = o_dtype == FGA_OUT_F32;
   const char* trace_file = std::getenv("FGA_TRACE");
-  if (trace_file != nullptr && cudaMalloc(&p.trace, 64 * FGA_TRACE_SLOTS * sizeof(long long)) == cudaSuccess)
-    cudaMemsetAsync(p.trace, 0, 64 * FGA_TRACE_SLOTS * sizeof(long long), stream);
+  if (trace_file != nullptr && cudaMalloc(&p.trace, FGA_TRACE_LEN * sizeof(long long)) == cudaSuccess)
+    cudaMemsetAsync(p.trace, 0, FGA_TRACE_LEN * sizeof(long long), stream);
   const char* which = std::getenv("FGA_ATTN_KERNEL");
+  if (const char* ti = std::getenv("FGA_TRACE_IT")) p.trace_it = std::atoi(ti);
   if (p.trace != nullptr) {
     int rc2 = (which != nullptr && std::strcmp(which, "sync") == 0)
                   ? launch_attn_sync(maps, p, static_cast<int>(D), f32, stream)
-                  : launch_attn_ws(maps, p, static_cast<int>(D), f32, stream);
-    long long host[64 * FGA_TRACE_SLOTS];
+                  : launch_attn_ws(maps, q, p, static_cast<int>(D), f32, stream);
+    static long long host[FGA_TRACE_LEN];
     cudaMemcpyAsync(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
     cudaFree(p.trace);
@@ -334,12 +335,18 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
         for (int k = 0; k < FGA_TRACE_SLOTS; ++k) std::fprintf(f, "%lld ", host[j * FGA_TRACE_SLOTS + k]);
         std::fprintf(f, "\n");
       }
+      for (int it = 0; it < 32; ++it) {
+        for (int k = 0; k < 8; ++k) std::fprintf(f, "%lld ", host[FGA_TRACE_TILE_OFF + it * 8 + k]);
+        std::fprintf(f, "\n");
+      }
+      for (int b = 0; b < 1024; ++b)
+        std::fprintf(f, "%lld %lld\n", host[FGA_TRACE_CTA_OFF + 2 * b], host[FGA_TRACE_CTA_OFF + 2 * b + 1]);
       std::fclose(f);
     }
     return rc2;
   }
   if (which != nullptr && std::strcmp(which, "sync") == 0) return launch_attn_sync(maps, p, static_cast<int>(D), f32, stream);
-  return launch_attn_ws(maps, p, static_cast<int>(D), f32, stream);
+  return launch_attn_ws(maps, q, p, static_cast<int>(D), f32, stream);
 }
 
 }  // namespace fga

@@ -1,8 +1,35 @@
+"""Summarise an FGA_TRACE timeline (development aid): python scripts/trace_report.py trace.txt"""
+import sys
+
 import numpy as np
-t = np.loadtxt('gpurun_out/trace.txt', dtype=np.int64)
-r = slice(5, 60)
-print("period", np.diff(t[r, 5]).mean())
-print(" mma: waitK", (t[r, 9] - t[r, 8]).mean(), "fence", (t[r, 13] - t[r, 9]).mean(), "S issue+commit", (t[r, 14] - t[r, 13]).mean())
+
+lines = open(sys.argv[1]).read().split("\n")
+t = np.array([[int(x) for x in l.split()] for l in lines[:64]], dtype=np.int64)
+tt = np.array([[int(x) for x in l.split()] for l in lines[64:96]], dtype=np.int64)
+cta = np.array([[int(x) for x in l.split()] for l in lines[96:] if l.strip()], dtype=np.int64)
+mm = t[:, 8] > 0
+j = np.nonzero(mm)[0]
+r = j[(j >= 4) & (j < j.max() - 2)]
+print("chunks traced", len(j), "MMA period per chunk (S issue)", (np.diff(t[r, 14]) / np.diff(r)).mean())
+print(" mma: waitK", (t[r, 9] - t[r, 8]).mean(), "fence", (t[r, 13] - t[r, 9]).mean(), "S issue+commit",
+      (t[r, 14] - t[r, 13]).mean())
 print(" mma: waitP", (t[r, 11] - t[r, 10]).mean(), "PV(wait V+fence+issue+commit)", (t[r, 12] - t[r, 11]).mean())
-print(" softmax: waitS", (t[r, 1] - t[r, 0]).mean(), "ld", (t[r, 2] - t[r, 1]).mean(), "max", (t[r, 3] - t[r, 2]).mean(),
-      "exp", (t[r, 4] - t[r, 3]).mean(), "st", (t[r, 5] - t[r, 4]).mean())
+sm = np.nonzero(t[:, 0] > 0)[0]
+s = sm[(sm >= 4) & (sm < sm.max() - 2)]
+print(" softmax(wg0) chunks", len(sm), "period per chunk", (np.diff(t[s, 5]) / np.diff(s)).mean() if len(s) > 1 else 0)
+print(" softmax: waitS", (t[s, 1] - t[s, 0]).mean(), "ld", (t[s, 2] - t[s, 1]).mean(), "max",
+      (t[s, 3] - t[s, 2]).mean(), "exp", (t[s, 4] - t[s, 3]).mean(), "st", (t[s, 5] - t[s, 4]).mean())
+
+# tile level (CTA 0): 0 Q issue, 1 MMA got Q, 2 MMA got o_empty (first PV), 3 MMA tile done, 4 epilogue start, 5 epilogue end
+v = tt[:, 1] > 0
+if v.any():
+    k = np.nonzero(v)[0]
+    print("tiles (CTA 0)", len(k), "tile period", np.diff(tt[k, 1]).mean() if len(k) > 1 else 0)
+    print(" per tile: Qissue->MMA got Q", (tt[k, 1] - tt[k, 0]).mean(), " MMA got Q->o_empty", (tt[k, 2] - tt[k, 1]).mean(),
+          " epilogue", (tt[k, 5] - tt[k, 4]).mean(), " lastPV issued->epi start", (tt[k, 4] - tt[k, 3]).mean())
+c = cta[cta[:, 0] > 0]
+if len(c):
+    t0 = c[:, 0].min()
+    d = (c[:, 1] - c[:, 0]) / 1e3
+    print(f"CTAs {len(c)}: start spread {(c[:, 0].max() - t0) / 1e3:.1f} us, duration min {d.min():.1f} "
+          f"median {np.median(d):.1f} max {d.max():.1f} us, end spread {(c[:, 1].max() - c[:, 1].min()) / 1e3:.1f} us")
