@@ -38,6 +38,10 @@ struct AttnParams {
 #define FGA_TRACE_TILE_OFF (64 * FGA_TRACE_SLOTS)
 #define FGA_TRACE_CTA_OFF (FGA_TRACE_TILE_OFF + 32 * 8)
 #define FGA_TRACE_LEN (FGA_TRACE_CTA_OFF + 2 * 1024)
+#ifndef FGA_TRACE_ON
+#define FGA_TRACE_ON 0  // timeline hooks are compiled in only for the trace build (scripts/trace_run.py)
+#endif
+#if FGA_TRACE_ON
 #define FGA_TS(p, it, j, slot)                                                                         \
   do {                                                                                                  \
     if ((p).trace != nullptr && blockIdx.x == 0 && (it) == (p).trace_it && (j) < 64)                    \
@@ -48,6 +52,14 @@ struct AttnParams {
     if ((p).trace != nullptr && blockIdx.x == 0 && (it) < 32)                                           \
       (p).trace[FGA_TRACE_TILE_OFF + (it) * 8 + (slot)] = clock64();                                    \
   } while (0)
+#else
+#define FGA_TS(p, it, j, slot) \
+  do {                         \
+  } while (0)
+#define FGA_TT(p, it, slot) \
+  do {                      \
+  } while (0)
+#endif
 __device__ __forceinline__ long long global_ns() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -166,16 +166,37 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
       }
       mbar_wait(&bar.kv_empty[slot], (use & 1) ^ 1);
       const char* src = kv ? gv : gk;
-      const uint32_t dst = kv_base + slot * L::KV + lane_off;
+      // opaque to the optimiser, so src + key * 2D stays one IMAD.WIDE.U32 per copy
+      asm volatile("mov.b64 %0, %0;" : "+l"(src));
+      // SW128 destination: row r's 16-byte chunk cc lands at r*128 + ((cc ^ (r & 7)) << 4).  This
+      // lane's rows are mm*RPI + sub (+32i), so (r & 7) cycles with period PER = 8 / RPI in mm and
+      // the address is dstb[mm % PER] + compile-time immediate.
+      constexpr int PER = 8 / RPI;
+      uint32_t dstb[PER];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {  // rows 32i .. 32i+31, keys held by keys[i]
-#pragma unroll 4
-        for (int mm = 0; mm < 32 / RPI; ++mm) {
-          const int rr = mm * RPI + sub;
-          const int key = __shfl_sync(0xffffffffu, keys[i], rr);
-          const int row = i * 32 + rr;
-          cp_async16(dst + row * 128 + ((cc ^ (row & 7)) << 4),
-                     key >= 0 ? src + static_cast<int64_t>(key) * (D * 2) : src, key >= 0 ? 16u : 0u);
+      for (int u = 0; u < PER; ++u)
+        dstb[u] = kv_base + slot * L::KV + lane_off + sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
+      if (c * BN + BN <= t.count) {
+        // full chunk: SHFL + IMAD.WIDE + LDGSTS per 16 bytes
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+          for (int mm = 0; mm < 32 / RPI; ++mm) {
+            const uint32_t key = static_cast<uint32_t>(__shfl_sync(0xffffffffu, keys[i], mm * RPI + sub));
+            const char* g = src + static_cast<size_t>(key) * (D * 2);
+            cp_async16_full(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, g);
+          }
+        }
+      } else {
+        // the tile's last chunk: rows past the list end are zero-filled
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+          for (int mm = 0; mm < 32 / RPI; ++mm) {
+            const int key = __shfl_sync(0xffffffffu, keys[i], mm * RPI + sub);
+            const char* g = src + static_cast<size_t>(static_cast<uint32_t>(max(key, 0))) * (D * 2);
+            cp_async16(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, g, key >= 0 ? 16u : 0u);
+          }
         }
       }
       cp_async_arrive_noinc(full);

@@ -96,6 +96,10 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
   asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
                : "memory");
 }
+// 16-byte cp.async (LDGSTS) without the zero-fill operand.
+__device__ __forceinline__ void cp_async16_full(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 // Arrive (without incrementing the pending count) on an mbarrier once all of
 // this thread's prior cp.async copies have landed.
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
