@@ -55,11 +55,18 @@ constexpr int NWARPS = WARP_PROD0 + NP;
 constexpr int REG_SOFTMAX = 184;
 constexpr int REG_OTHER = 72;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units (factor 256)
+constexpr float RESCALE_SUM = 256.0f;      // 2^RESCALE_THRESHOLD
 constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
 #ifndef FGA_POLY_EVERY
-#define FGA_POLY_EVERY 4
+#define FGA_POLY_EVERY (1 << 20)
 #endif
 constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the FMA pipe (MUFU relief)
+#ifndef FGA_POLY_DEG
+#define FGA_POLY_DEG 3
+#endif
+#ifndef FGA_EXP_H2
+#define FGA_EXP_H2 0
+#endif
 
 template <int D>
 struct WsSmem {
@@ -314,6 +321,39 @@ __device__ __forceinline__ void write_q(const AttnParams& p, const void* qptr, c
   }
 }
 
+// P = 2^(s*scale*log2e - m) for this thread's 2 rows x 32 scores: packed FFMA2 for the
+// argument, MUFU ex2 for most pairs and the FMA-pipe polynomial for 1 in POLY_EVERY pairs,
+// packed FADD2 row sums, bf16 pairs in the 16x128b register order.
+__device__ __forceinline__ void exp_chunk(const uint32_t (&sv)[2][32], float sl2, const float (&m_use)[2],
+                                          uint32_t (&pk)[32], float2 (&sum2)[2][2]) {
+  const float2 sc2 = make_float2(sl2, sl2);
+  const float2 nm[2] = {make_float2(-m_use[0], -m_use[0]), make_float2(-m_use[1], -m_use[1])};
+#pragma unroll
+  for (int r = 0; r < 2; ++r) sum2[r][0] = sum2[r][1] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const float2 sx = make_float2(__uint_as_float(sv[hh][4 * k + 2 * r]), __uint_as_float(sv[hh][4 * k + 2 * r + 1]));
+        const float2 x = __ffma2_rn(sx, sc2, nm[r]);
+        float2 pr;
+        if (FGA_EXP_H2) {
+          pr = ex2_h2(x);
+        } else if (((8 * hh + k) * 2 + r) % POLY_EVERY == POLY_EVERY - 1) {
+          pr = ex2_poly2<FGA_POLY_DEG>(x);
+        } else {
+          pr.x = ex2(x.x);
+          pr.y = ex2(x.y);
+        }
+        sum2[r][k & 1] = __fadd2_rn(sum2[r][k & 1], pr);
+        pk[2 * (8 * hh + k) + r] = pack_bf16(pr.x, pr.y);
+      }
+    }
+  }
+}
+
 template <int D, bool OUT_F32>
 __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, const Bars& bar, uint32_t tmem, int tid,
                                         float* xch) {
@@ -361,65 +401,50 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
                 sv[hh][4 * k + 2 + e] = __float_as_uint(-INFINITY);
               }
       }
-      // row max: 32 scores per row per thread (FMNMX3 chains), then over the quad
-      float rmax[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        float mh[2];
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          // the 16 values of row r in this half: sv[hh][4*(i/2) + 2r + i%2], i = 0..15
-#define FGA_SV(i) __uint_as_float(sv[hh][4 * ((i) >> 1) + 2 * r + ((i) & 1)])
-          float m = fmax3f(FGA_SV(0), FGA_SV(1), FGA_SV(2));
-#pragma unroll
-          for (int i = 3; i < 15; i += 2) m = fmax3f(m, FGA_SV(i), FGA_SV(i + 1));
-          mh[hh] = fmaxf(m, FGA_SV(15));
-#undef FGA_SV
-        }
-        float m = fmaxf(mh[0], mh[1]);
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-        rmax[r] = m * sl2;
-      }
-      if (tr) FGA_TS(p, it, j, 3);
+      // Fast path (every chunk after the first): P with the current running max -- no row max,
+      // no quad shuffles.  A score above the running max by more than RESCALE_THRESHOLD shows
+      // up as a partial row sum above 2^THRESHOLD (all terms are positive), which sends the
+      // warp to the slow path: quad-reduced row max, new running max (O rescaled), P recomputed.
       float alpha[2] = {1.f, 1.f};
       bool rescale = false;
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        if (j == 0) {
-          m_use[r] = rmax[r];
-        } else if (rmax[r] - m_use[r] > RESCALE_THRESHOLD) {
-          alpha[r] = ex2(m_use[r] - rmax[r]);
-          m_use[r] = rmax[r];
-          rescale = true;
-        }
-      }
-      // P = 2^(s*scale*log2e - m): packed FFMA2 for the argument, MUFU ex2 for most
-      // pairs and the FMA-pipe polynomial for 1 in POLY_EVERY pairs, packed FADD2 sums
-      const float2 sc2 = make_float2(sl2, sl2);
-      const float2 nm[2] = {make_float2(-m_use[0], -m_use[0]), make_float2(-m_use[1], -m_use[1])};
-      float2 sum2[2][2] = {{make_float2(0.f, 0.f), make_float2(0.f, 0.f)}, {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}};
       uint32_t pk[32];  // 16x128b: pk[2K + r] = (row r0 + 8r, P col 4K + a), K = 8*half + k
+      float2 sum2[2][2];
+      bool slow = j == 0;
+      if (!slow) {
+        exp_chunk(sv, sl2, m_use, pk, sum2);
+        const float2 u0 = __fadd2_rn(sum2[0][0], sum2[0][1]), u1 = __fadd2_rn(sum2[1][0], sum2[1][1]);
+        const bool over = !(u0.x + u0.y <= RESCALE_SUM) || !(u1.x + u1.y <= RESCALE_SUM);
+        slow = __any_sync(0xffffffffu, over);
+      }
+      if (slow) {
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+        for (int r = 0; r < 2; ++r) {
+          float mh[2];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+          for (int hh = 0; hh < 2; ++hh) {
+            // the 16 values of row r in this half: sv[hh][4*(i/2) + 2r + i%2], i = 0..15
+#define FGA_SV(i) __uint_as_float(sv[hh][4 * ((i) >> 1) + 2 * r + ((i) & 1)])
+            float m = fmax3f(FGA_SV(0), FGA_SV(1), FGA_SV(2));
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const float2 sx = make_float2(__uint_as_float(sv[hh][4 * k + 2 * r]), __uint_as_float(sv[hh][4 * k + 2 * r + 1]));
-            const float2 x = __ffma2_rn(sx, sc2, nm[r]);
-            float2 pr;
-            if (((8 * hh + k) * 2 + r) % POLY_EVERY == POLY_EVERY - 1) {
-              pr = ex2_poly2(x);
-            } else {
-              pr.x = ex2(x.x);
-              pr.y = ex2(x.y);
-            }
-            sum2[r][k & 1] = __fadd2_rn(sum2[r][k & 1], pr);
-            pk[2 * (8 * hh + k) + r] = pack_bf16(pr.x, pr.y);
+            for (int i = 3; i < 15; i += 2) m = fmax3f(m, FGA_SV(i), FGA_SV(i + 1));
+            mh[hh] = fmaxf(m, FGA_SV(15));
+#undef FGA_SV
+          }
+          float m = fmaxf(mh[0], mh[1]);
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+          const float rmax = m * sl2;
+          if (j == 0) {
+            m_use[r] = rmax;
+          } else if (rmax - m_use[r] > RESCALE_THRESHOLD) {
+            alpha[r] = ex2(m_use[r] - rmax);
+            m_use[r] = rmax;
+            rescale = true;
           }
         }
+        exp_chunk(sv, sl2, m_use, pk, sum2);
       }
+      if (tr) FGA_TS(p, it, j, 3);
       tmem_st16x128_x16(tS, pk);
       if (tr) FGA_TS(p, it, j, 4);
 #pragma unroll

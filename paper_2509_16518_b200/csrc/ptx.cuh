@@ -273,6 +273,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
 // 2^x for a pair on the FMA pipe with packed f32x2 ops (FFMA2/FADD2): same
 // cubic as ex2_poly; the exponent add needs no bias because
 // (0x4B400000 << 23) == 0 mod 2^32.
+template <int DEG = 3>
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   x.x = fmaxf(x.x, -127.f);  // -inf (masked column) -> exactly 0
   x.y = fmaxf(x.y, -127.f);
@@ -280,11 +281,27 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 t = __fadd2_rn(x, magic);
   const float2 u = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
   const float2 f = __ffma2_rn(u, make_float2(-1.f, -1.f), x);  // x - round(x)
-  float2 p = __ffma2_rn(f, make_float2(0.0550141495f, 0.0550141495f), make_float2(0.2422112540f, 0.2422112540f));
-  p = __ffma2_rn(p, f, make_float2(0.6932820230f, 0.6932820230f));
-  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  float2 p;
+  if constexpr (DEG == 3) {  // max rel. error 1.0e-4
+    p = __ffma2_rn(f, make_float2(0.0550141495f, 0.0550141495f), make_float2(0.2422112540f, 0.2422112540f));
+    p = __ffma2_rn(p, f, make_float2(0.6932820230f, 0.6932820230f));
+    p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  } else {  // quadratic minimax, max rel. error 1.7e-3 (below bf16's 3.9e-3 rounding of P)
+    p = __ffma2_rn(f, make_float2(0.23842697f, 0.23842697f), make_float2(0.7034453f, 0.7034453f));
+    p = __ffma2_rn(p, f, make_float2(1.00044307f, 1.00044307f));
+  }
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+// 2^x for a pair through the half-precision MUFU path (one ex2.approx.f16x2 per pair):
+// x <= 8 here, rounded to f16 (abs. error <= 2^-8 for |x| < 8, i.e. <= 0.27% relative in 2^x).
+__device__ __forceinline__ float2 ex2_h2(float2 x) {
+  uint32_t h;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x.y), "f"(x.x));
+  asm("ex2.approx.f16x2 %0, %0;" : "+r"(h));
+  float2 r;
+  asm("{\n.reg .f16 l, u;\nmov.b32 {l, u}, %2;\ncvt.f32.f16 %0, l;\ncvt.f32.f16 %1, u;\n}" : "=f"(r.x), "=f"(r.y) : "r"(h));
+  return r;
 }
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   float m;

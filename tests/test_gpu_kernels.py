@@ -190,6 +190,39 @@ def test_unsorted_duplicate_free_lists_and_stride(d):
     assert np.abs(o.cpu().numpy() - ref).max() <= ATOL
 
 
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("order", ["ascending", "descending"])
+def test_online_rescale_large_dynamic_range(d, order):
+    # scores grow by ~50 log2 units along the key list, so the running max moves many times
+    # (the kernel's lazy-rescale slow path) -- or, descending, never after the first chunk
+    b, h, n, m = 1, 2, 1536, 128
+    rng = np.random.default_rng(11 + d)
+    q = oracle.bf16_round(4.0 * rng.standard_normal((b, h, n, d)).astype(np.float32))
+    ramp = (0.2 + 3.0 * np.arange(n) / n).astype(np.float32)
+    k = oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32) * ramp[None, None, :, None])
+    v = oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32))
+    lists = oracle.random_lists(b, h, n, m, 0.6, seed=d)
+    ref = oracle.masked_attention(q, k, v, lists, m)
+    g = oracle.num_groups(n, m)
+    pad = np.full((b * h * g, n), -1, np.int32)
+    counts = np.zeros(b * h * g, np.int32)
+    for i, lst in enumerate(lists):
+        lst = np.asarray(lst)[::-1] if order == "descending" else np.asarray(lst)
+        pad[i, : len(lst)] = lst
+        counts[i] = len(lst)
+    o, lse = run_sparse(to_bf16_dev(q), to_bf16_dev(k), to_bf16_dev(v), torch.from_numpy(pad).cuda(),
+                        torch.from_numpy(counts).cuda(), b, h, n, d, m, lse=True)
+    assert np.isfinite(o.cpu().numpy()).all()
+    assert np.abs(o.cpu().numpy() - ref).max() <= ATOL
+    lse = lse.cpu().numpy()
+    for i, lst in enumerate(lists):
+        bb, hh, gg = i // (h * g), (i // g) % h, i % g
+        lo, hi = gg * m, min(gg * m + m, n)
+        sc = (q[bb, hh, lo:hi].astype(np.float64) @ k[bb, hh, lst].astype(np.float64).T) / np.sqrt(d)
+        ref_l = np.log(np.exp(sc - sc.max(1, keepdims=True)).sum(1)) + sc.max(1)
+        assert np.abs(lse[bb, hh, lo:hi] - ref_l).max() < 2e-2
+
+
 @pytest.mark.parametrize("m", [16, 64, 200, 256])
 def test_group_sizes(m):
     b, h, n, d = 1, 2, 600, 64
