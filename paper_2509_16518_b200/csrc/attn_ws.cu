@@ -61,6 +61,12 @@ constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
 #define FGA_POLY_EVERY (1 << 20)
 #endif
 constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the FMA pipe (MUFU relief)
+#ifndef FGA_NOGATHER
+#define FGA_NOGATHER 0  // timing experiments only
+#endif
+#ifndef FGA_NOEXP
+#define FGA_NOEXP 0  // timing experiments only
+#endif
 #ifndef FGA_POLY_DEG
 #define FGA_POLY_DEG 3
 #endif
@@ -183,7 +189,9 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
 #pragma unroll
       for (int u = 0; u < PER; ++u)
         dstb[u] = kv_base + slot * L::KV + lane_off + sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
-      if (c * BN + BN <= t.count) {
+      if (FGA_NOGATHER) {
+        // timing experiment only: no data movement
+      } else if (c * BN + BN <= t.count) {
         // full chunk: SHFL + IMAD.WIDE + LDGSTS per 16 bytes
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -409,8 +417,13 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
       bool rescale = false;
       uint32_t pk[32];  // 16x128b: pk[2K + r] = (row r0 + 8r, P col 4K + a), K = 8*half + k
       float2 sum2[2][2];
-      bool slow = j == 0;
-      if (!slow) {
+      bool slow = j == 0 && !FGA_NOEXP;
+      if (FGA_NOEXP) {  // timing experiment only: P = S bits, no exp
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pk[i] = sv[i >> 4][i & 15];
+        sum2[0][0] = sum2[0][1] = sum2[1][0] = sum2[1][1] = make_float2(1.f, 1.f);
+        if (j == 0) m_use[0] = m_use[1] = 0.f;
+      } else if (!slow) {
         exp_chunk(sv, sl2, m_use, pk, sum2);
         const float2 u0 = __fadd2_rn(sum2[0][0], sum2[0][1]), u1 = __fadd2_rn(sum2[1][0], sum2[1][1]);
         const bool over = !(u0.x + u0.y <= RESCALE_SUM) || !(u1.x + u1.y <= RESCALE_SUM);

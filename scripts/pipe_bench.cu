@@ -42,6 +42,28 @@ __global__ void kern(float* out, long long* cyc, int iters) {
       } else if (MODE == 5) {  // truncating pack: PRMT only
         acc += __byte_perm(__float_as_uint(a[i]), __float_as_uint(a[i + 1]), 0x7632);
         a[i] = __uint_as_float(__float_as_uint(a[i]) + 1);
+      } else if (MODE == 7) {  // 2 MUFU + 1 FFMA2 (independent)
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i + 1]));
+        float2 x = make_float2(a[(i + 4) & 15], a[(i + 5) & 15]);
+        x = __ffma2_rn(x, make_float2(1.0001f, 1.0001f), make_float2(0.5f, 0.5f));
+        a[(i + 4) & 15] = x.x; a[(i + 5) & 15] = x.y;
+      } else if (MODE == 8) {  // 2 MUFU + 2 FFMA (scalar, independent)
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i + 1]));
+        a[(i + 4) & 15] = fmaf(a[(i + 4) & 15], 1.0001f, 0.5f);
+        a[(i + 5) & 15] = fmaf(a[(i + 5) & 15], 1.0001f, 0.5f);
+      } else if (MODE == 9) {  // 2 MUFU + 2 FFMA2 + 1 F2FP (the softmax pair mix)
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i]));
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[i + 1]));
+        float2 x = make_float2(a[(i + 4) & 15], a[(i + 5) & 15]);
+        x = __ffma2_rn(x, make_float2(1.0001f, 1.0001f), make_float2(0.5f, 0.5f));
+        float2 y = make_float2(a[(i + 8) & 15], a[(i + 9) & 15]);
+        y = __fadd2_rn(y, make_float2(0.5f, 0.5f));
+        a[(i + 4) & 15] = x.x; a[(i + 5) & 15] = x.y; a[(i + 8) & 15] = y.x; a[(i + 9) & 15] = y.y;
+        uint32_t r;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a[i]), "f"(a[i + 1]));
+        acc += r;
       } else if (MODE == 6) {  // 1 FMNMX3
         float m;
         asm volatile("max.f32 %0, %1, %2, %3;" : "=f"(m) : "f"(a[i]), "f"(a[i + 1]), "f"(a[(i + 2) & 15]));
@@ -81,6 +103,9 @@ int main() {
     run<4>("int RNE pack (~8 instr)", w, 8);
     run<5>("PRMT pack + IADD", w, 2);
     run<6>("FMNMX3", w, 1);
+    run<7>("2 MUFU + 1 FFMA2 (per 3)", w, 3);
+    run<8>("2 MUFU + 2 FFMA (per 4)", w, 4);
+    run<9>("2 MUFU+FFMA2+FADD2+F2FP (per 5)", w, 5);
   }
   return 0;
 }

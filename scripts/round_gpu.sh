@@ -1,9 +1,11 @@
 #!/bin/bash
-# Round GPU pass: parity tests, smoke, probe, bench line, ncu launch list.
+# Round GPU pass: parity tests, smoke, bench line, ncu launch list + full capture of the attention kernel.
 set -u
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
-timeout -s KILL 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout -s KILL 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log
-timeout -s KILL 200 python scripts/probe_perf.py 12 > gpurun_out/probe.log 2>&1; cat gpurun_out/probe.log
-timeout -s KILL 400 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -c 3000 gpurun_out/bench.json
+timeout -s KILL 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
+timeout -s KILL 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
+timeout -s KILL 200 python scripts/probe_perf.py 12 > gpurun_out/probe.log 2>&1; cat gpurun_out/probe.log | grep -E "sparse|sdpa|speedup"
+timeout -s KILL 500 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -c 600 gpurun_out/bench.json
+timeout -s KILL 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; tail -c 300 gpurun_out/bench_ref.json
+if [ "${NCU:-1}" = 1 ]; then ./scripts/ncu_attn.sh 0.45; fi
