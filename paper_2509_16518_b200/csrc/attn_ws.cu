@@ -48,10 +48,11 @@ namespace fga {
 namespace {
 
 constexpr int NSOFT = 8;        // softmax warps
-constexpr int WARP_MMA = 8;
-constexpr int WARP_PROD0 = 9;
-constexpr int NP = 7;           // item producer warps
-constexpr int NWARPS = WARP_PROD0 + NP;
+constexpr int WARP_S = 8;       // issuer of S = Q K^T
+constexpr int WARP_PV = 9;      // issuer of O += P V
+constexpr int WARP_PROD0 = 10;
+constexpr int NPR = 3;          // producer warps per ring (K ring, V ring)
+constexpr int NWARPS = WARP_PROD0 + 2 * NPR;
 constexpr int REG_SOFTMAX = 184;
 constexpr int REG_OTHER = 72;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units (factor 256)
@@ -76,22 +77,26 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 
 template <int D>
 struct WsSmem {
-  static constexpr int KV = (D / 64) * HALF;  // one K or V chunk
-  static constexpr int NSLOT = D == 128 ? 7 : 13;
-  static constexpr int OFF_KV = 0;
-  static constexpr int OFF_BAR = OFF_KV + NSLOT * KV;
-  static constexpr int NBAR = 2 * NSLOT + 2 + 2 + 2 + 3;
+  static constexpr int KV = (D / 64) * HALF;       // one K or V chunk
+  static constexpr int NSK = D == 128 ? 4 : 7;     // K ring slots
+  static constexpr int NSV = D == 128 ? 3 : 6;     // V ring slots
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + NSK * KV;
+  static constexpr int OFF_BAR = OFF_V + NSV * KV;
+  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3;
   static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row
   static constexpr int BYTES = OFF_XCH + 2 * 128 * 4;
-  static_assert(NP <= NSLOT, "more producer warps than ring slots breaks the empty-barrier parity");
+  static_assert(NPR <= NSK && NPR <= NSV, "more producer warps than ring slots breaks the empty-barrier parity");
 };
 
 struct Bars {
-  uint64_t* kv_full;   // [NSLOT] count 32 (one producer warp)
-  uint64_t* kv_empty;  // [NSLOT] MMA commit
+  uint64_t* k_full;    // [NSK] count 32 (one producer warp)
+  uint64_t* k_empty;   // [NSK] S-issuer commit
+  uint64_t* v_full;    // [NSV]
+  uint64_t* v_empty;   // [NSV] PV-issuer commit
   uint64_t* s_full;    // [2]
   uint64_t* p_full;    // [2] count 8 (every softmax warp)
-  uint64_t* pv_done;   // [2]
+  uint64_t* pv_done;   // [2] completion of PV into S buffer b's P
   uint64_t* q_full;    // count 8 (every softmax warp writes a part of Q)
   uint64_t* o_full;
   uint64_t* o_empty;   // count 8
@@ -103,9 +108,11 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   using L = WsSmem<D>;
   uint64_t* b = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   Bars r;
-  r.kv_full = b;
-  r.kv_empty = b + L::NSLOT;
-  r.s_full = r.kv_empty + L::NSLOT;
+  r.k_full = b;
+  r.k_empty = r.k_full + L::NSK;
+  r.v_full = r.k_empty + L::NSK;
+  r.v_empty = r.v_full + L::NSV;
+  r.s_full = r.v_empty + L::NSV;
   r.p_full = r.s_full + 2;
   r.pv_done = r.p_full + 2;
   r.q_full = r.pv_done + 2;
@@ -115,57 +122,46 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   return r;
 }
 
-// Ring items of a tile with n chunks, in MMA consumption order:
-//   K0, K1, V0, K2, V1, ..., K_{n-1}, V_{n-2}, V_{n-1}
-__device__ __forceinline__ uint32_t item_of_k(int c) { return c == 0 ? 0u : 2u * c - 1u; }
-__device__ __forceinline__ uint32_t item_of_v(int c, int n) { return c < n - 1 ? 2u * c + 2u : 2u * n - 1u; }
-
 // ------------------------------------------------------------------ producers
-// Producer warp pw packs ring items pw, pw+NP, ...  Each lane holds 4 of the
-// chunk's 128 keys (loaded before the slot wait); one warp instruction copies
-// RPI rows (LPR lanes x 16 B per row) into the SW128 slot.  Rows past the list
-// end are zero-filled (src-size 0), so no stale or NaN bytes reach the MMA.
-// NP <= NSLOT keeps the empty-barrier parity unambiguous (the MMA frees slots
-// in item order).
+// Two rings, each filled and drained in chunk order: ring kv = 0 holds K chunks
+// (freed by the S issuer), ring kv = 1 holds V chunks (freed by the PV issuer).
+// Producer warp w of a ring packs the ring's chunks w, w+NPR, ... (CTA-wide
+// chunk order).  Each lane holds 4 of the chunk's 128 keys (loaded before the
+// slot wait); one warp instruction copies RPI rows (LPR lanes x 16 B per row).
+// Rows past the list end are zero-filled (src-size 0), so no stale or NaN bytes
+// reach the MMA.  NPR <= ring slots keeps the empty-barrier parity unambiguous.
 template <int D>
 __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
-                                         uint8_t* smem, const Bars& bar, int pw, int lane) {
+                                         uint8_t* smem, const Bars& bar, int kv, int pw, int lane) {
   using L = WsSmem<D>;
   constexpr int LPR = D / 8;     // lanes per 2*D-byte row
   constexpr int RPI = 32 / LPR;  // rows per warp instruction
+  const int nslot = kv ? L::NSV : L::NSK;
   const uint64_t pol_kv = policy_evict_last();
   const int sub = lane / LPR, ch = lane % LPR;
   const uint32_t lane_off = static_cast<uint32_t>((ch >> 3) * HALF);
   const int cc = ch & 7;
-  const uint32_t kv_base = smem_u32(smem + L::OFF_KV);
-  uint32_t base = 0;  // CTA-wide index of the tile's first item
+  uint8_t* ring = smem + (kv ? L::OFF_V : L::OFF_K);
+  const uint32_t ring_base = smem_u32(ring);
+  uint64_t* fullb = kv ? bar.v_full : bar.k_full;
+  uint64_t* emptyb = kv ? bar.v_empty : bar.k_empty;
+  const CUtensorMap* tm = kv ? tmV2 : tmK2;
+  uint32_t base = 0;  // CTA-wide index of the tile's first chunk
   for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
     const Tile t = decode_tile(p, tile);
-    const uint32_t ni = 2u * static_cast<uint32_t>(t.nchunks);
-    const char* gk = static_cast<const char*>(p.k) + static_cast<int64_t>(t.row0) * (D * 2) + ch * 16;
-    const char* gv = static_cast<const char*>(p.v) + static_cast<int64_t>(t.row0) * (D * 2) + ch * 16;
-    for (uint32_t item = base + (static_cast<uint32_t>(pw) + NP - base % NP) % NP; item < base + ni; item += NP) {
-      const uint32_t li = item - base;
-      int kv, c;
-      if (li == 0) {
-        kv = 0; c = 0;
-      } else if (li == ni - 1) {
-        kv = 1; c = t.nchunks - 1;
-      } else if (li & 1u) {
-        kv = 0; c = static_cast<int>((li + 1) >> 1);
-      } else {
-        kv = 1; c = static_cast<int>((li - 2) >> 1);
-      }
-      const uint32_t slot = item % L::NSLOT, use = item / L::NSLOT;
-      uint64_t* full = &bar.kv_full[slot];
+    const uint32_t n = static_cast<uint32_t>(t.nchunks);
+    const char* gsrc = static_cast<const char*>(kv ? p.v : p.k) + static_cast<int64_t>(t.row0) * (D * 2) + ch * 16;
+    for (uint32_t item = base + (static_cast<uint32_t>(pw) + NPR - base % NPR) % NPR; item < base + n; item += NPR) {
+      const int c = static_cast<int>(item - base);
+      const uint32_t slot = item % nslot, use = item / nslot;
+      uint64_t* full = &fullb[slot];
       if (p.dense) {
-        mbar_wait(&bar.kv_empty[slot], (use & 1) ^ 1);
+        mbar_wait(&emptyb[slot], (use & 1) ^ 1);
         if (lane == 0) {
           mbar_expect_tx(full, BN * D * 2);
 #pragma unroll
           for (int h = 0; h < D / 64; ++h)
-            tma_load_2d(smem + L::OFF_KV + slot * L::KV + h * HALF, kv ? tmV2 : tmK2, full, h * 64, t.row0 + c * BN,
-                        pol_kv);
+            tma_load_2d(ring + slot * L::KV + h * HALF, tm, full, h * 64, t.row0 + c * BN, pol_kv);
         } else {
           mbar_arrive(full);
         }
@@ -177,8 +173,8 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
         const int row = c * BN + i * 32 + lane;
         keys[i] = row < t.count ? __ldg(t.list + row) : -1;
       }
-      mbar_wait(&bar.kv_empty[slot], (use & 1) ^ 1);
-      const char* src = kv ? gv : gk;
+      mbar_wait(&emptyb[slot], (use & 1) ^ 1);
+      const char* src = gsrc;
       // opaque to the optimiser, so src + key * 2D stays one IMAD.WIDE.U32 per copy
       asm volatile("mov.b64 %0, %0;" : "+l"(src));
       // SW128 destination: row r's 16-byte chunk cc lands at r*128 + ((cc ^ (r & 7)) << 4).  This
@@ -188,7 +184,7 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
       uint32_t dstb[PER];
 #pragma unroll
       for (int u = 0; u < PER; ++u)
-        dstb[u] = kv_base + slot * L::KV + lane_off + sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
+        dstb[u] = ring_base + slot * L::KV + lane_off + sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
       if (FGA_NOGATHER) {
         // timing experiment only: no data movement
       } else if (c * BN + BN <= t.count) {
@@ -216,86 +212,99 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
       }
       cp_async_arrive_noinc(full);
     }
-    base += ni;
+    base += n;
   }
 }
 
-// ------------------------------------------------------------------ MMA issuer (one warp)
-// The whole warp runs the loop (waits, descriptor arithmetic stay warp-uniform);
-// one elected lane issues each batch of tcgen05.mma + commits.
+// ------------------------------------------------------------------ MMA issuers
+// Two warps feed the tensor core so one's barrier waits overlap the other's
+// issue (a tcgen05.mma issue stalls until the MMA unit takes it, so a single
+// issuer leaves the unit idle across every wait).  In each warp the loop is
+// warp-uniform and one elected lane issues.  Ordering between them is by
+// completion barriers only: S_c reuses the TMEM buffer whose P_{c-2} feeds
+// PV_{c-2}, so the S issuer waits for PV_{c-2} to complete (pv_done).
 template <int D>
-__device__ __forceinline__ void mma_issuer(const AttnParams& p, uint8_t* smem, const Bars& bar, uint32_t tmem) {
+__device__ __forceinline__ void s_issuer(const AttnParams& p, uint8_t* smem, const Bars& bar, uint32_t tmem) {
   using L = WsSmem<D>;
   constexpr uint32_t IDESC_S = idesc_bf16(BM, BN, false, false);  // Q (TMEM), K K-major
-  constexpr uint32_t IDESC_O = idesc_bf16(BM, D, false, true);    // P (TMEM), V MN-major
-  // descriptor templates; the start-address field (addr >> 4) is advanced by adding offset >> 4
-  const uint64_t dk0 = sdesc_sw128(smem_u32(smem + L::OFF_KV), 16, 1024);
-  const uint64_t dv0 = sdesc_sw128(smem_u32(smem + L::OFF_KV), HALF, 1024);
-  const uint32_t tQ = tmem + TM_Q, tO = tmem + TM_O;
-  uint32_t chunk = 0, base = 0;
+  const uint64_t dk0 = sdesc_sw128(smem_u32(smem + L::OFF_K), 16, 1024);
+  const uint32_t tQ = tmem + TM_Q;
+  uint32_t c = 0, slot = 0, use = 0;  // CTA-wide chunk counter, K ring position
   int it = 0;
   for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
-    const int n = t.nchunks;
-    mbar_wait(bar.q_full, it & 1);
-    FGA_TT(p, it, 1);
-    tc_fence_after();
-    for (int j = 0; j <= n; ++j) {
-      if (j < n) {
-        const uint32_t c = chunk + j;
-        const uint32_t item = base + item_of_k(j), slot = item % L::NSLOT, use = item / L::NSLOT;
-        FGA_TS(p, it, j, 8);
-        mbar_wait(&bar.kv_full[slot], use & 1);
-        FGA_TS(p, it, j, 9);
-        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
-        tc_fence_after();
-        FGA_TS(p, it, j, 13);
-        const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
-        const uint32_t tS = tmem + TM_S + (c & 1) * 128;
-        if (elect_one()) {
+    if (t.nchunks > 0) {
+      mbar_wait(bar.q_full, it & 1);
+      FGA_TT(p, it, 1);
+    }
+    for (int j = 0; j < t.nchunks; ++j, ++c) {
+      FGA_TS(p, it, j, 8);
+      if (c >= 2) mbar_wait(&bar.pv_done[c & 1], ((c - 2) >> 1) & 1);  // S[c&1] free (PV_{c-2} done)
+      mbar_wait(&bar.k_full[slot], use & 1);
+      FGA_TS(p, it, j, 9);
+      fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
+      tc_fence_after();
+      const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
+      const uint32_t tS = tmem + TM_S + (c & 1) * 128;
+      if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
-            umma_ts(tS, tQ + kk * 8, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&bar.s_full[c & 1]);
-          umma_commit(&bar.kv_empty[slot]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
+          umma_ts(tS, tQ + kk * 8, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
         }
-        __syncwarp();
-        FGA_TS(p, it, j, 14);
+        umma_commit(&bar.s_full[c & 1]);
+        umma_commit(&bar.k_empty[slot]);
       }
-      if (j >= 1) {
-        const uint32_t c = chunk + j - 1;
-        if (j == 1) {
-          mbar_wait(bar.o_empty, (it & 1) ^ 1);  // previous tile's epilogue has read O
-          FGA_TT(p, it, 2);
-          tc_fence_after();
-        }
-        FGA_TS(p, it, j - 1, 10);
-        mbar_wait(&bar.p_full[c & 1], (c >> 1) & 1);
-        FGA_TS(p, it, j - 1, 11);
-        const uint32_t item = base + item_of_v(j - 1, n), slot = item % L::NSLOT, use = item / L::NSLOT;
-        mbar_wait(&bar.kv_full[slot], use & 1);
-        fence_proxy_async_smem();
-        tc_fence_after();
-        const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
-        const uint32_t tP = tmem + TM_S + (c & 1) * 128;
-        if (elect_one()) {
+      __syncwarp();
+      FGA_TS(p, it, j, 14);
+      if (++slot == L::NSK) {
+        slot = 0;
+        ++use;
+      }
+    }
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void pv_issuer(const AttnParams& p, uint8_t* smem, const Bars& bar, uint32_t tmem) {
+  using L = WsSmem<D>;
+  constexpr uint32_t IDESC_O = idesc_bf16(BM, D, false, true);  // P (TMEM), V MN-major
+  const uint64_t dv0 = sdesc_sw128(smem_u32(smem + L::OFF_V), HALF, 1024);
+  const uint32_t tO = tmem + TM_O;
+  uint32_t c = 0, slot = 0, use = 0;
+  int it = 0;
+  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+    const Tile t = decode_tile(p, tile);
+    for (int j = 0; j < t.nchunks; ++j, ++c) {
+      if (j == 0) {
+        mbar_wait(bar.o_empty, (it & 1) ^ 1);  // previous tile's epilogue has read O
+        FGA_TT(p, it, 2);
+      }
+      FGA_TS(p, it, j, 10);
+      mbar_wait(&bar.p_full[c & 1], (c >> 1) & 1);
+      FGA_TS(p, it, j, 11);
+      mbar_wait(&bar.v_full[slot], use & 1);
+      fence_proxy_async_smem();
+      tc_fence_after();
+      const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
+      const uint32_t tP = tmem + TM_S + (c & 1) * 128;
+      if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
-            umma_ts(tO, tP + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, (j > 1 || kk > 0) ? 1u : 0u);
-          umma_commit(&bar.kv_empty[slot]);
-          umma_commit(&bar.pv_done[c & 1]);
-        }
-        __syncwarp();
-        FGA_TS(p, it, j - 1, 12);
+        for (int kk = 0; kk < BN / 16; ++kk)
+          umma_ts(tO, tP + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&bar.v_empty[slot]);
+        umma_commit(&bar.pv_done[c & 1]);
+      }
+      __syncwarp();
+      FGA_TS(p, it, j, 12);
+      if (++slot == L::NSV) {
+        slot = 0;
+        ++use;
       }
     }
     if (elect_one()) umma_commit(bar.o_full);
     __syncwarp();
     FGA_TT(p, it, 3);
-    chunk += n;
-    base += 2u * n;
   }
 }
 
@@ -555,9 +564,13 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
       prefetch_tmap(&tmK2);
       prefetch_tmap(&tmV2);
     }
-    for (int i = 0; i < L::NSLOT; ++i) {
-      mbar_init(&bar.kv_full[i], 32);  // one producer warp per item
-      mbar_init(&bar.kv_empty[i], 1);
+    for (int i = 0; i < L::NSK; ++i) {
+      mbar_init(&bar.k_full[i], 32);  // one producer warp per chunk
+      mbar_init(&bar.k_empty[i], 1);
+    }
+    for (int i = 0; i < L::NSV; ++i) {
+      mbar_init(&bar.v_full[i], 32);
+      mbar_init(&bar.v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar.s_full[i], 1);
@@ -590,10 +603,13 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     softmax<D, OUT_F32>(p, qptr, bar, tmem, tid, reinterpret_cast<float*>(smem + L::OFF_XCH));
   } else {
     setmaxnreg_dec<REG_OTHER>();
-    if (warp == WARP_MMA) {
-      mma_issuer<D>(p, smem, bar, tmem);
+    if (warp == WARP_S) {
+      s_issuer<D>(p, smem, bar, tmem);
+    } else if (warp == WARP_PV) {
+      pv_issuer<D>(p, smem, bar, tmem);
     } else {
-      producer<D>(p, &tmK2, &tmV2, smem, bar, warp - WARP_PROD0, lane);
+      const int w = warp - WARP_PROD0;
+      producer<D>(p, &tmK2, &tmV2, smem, bar, w / NPR, w % NPR, lane);
     }
   }
   tc_fence_before();
