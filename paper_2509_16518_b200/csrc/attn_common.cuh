@@ -93,28 +93,34 @@ __device__ __forceinline__ Tile decode_tile(const AttnParams& p, int64_t tile) {
   return t;
 }
 
-// Store 32 fp32 accumulator columns (scaled) of one output row.
-template <bool OUT_F32>
-__device__ __forceinline__ void store_row32(void* out, int64_t off, const uint32_t (&o)[32], float scale) {
+// Store N (multiple of 8) fp32 accumulator columns (scaled) of one output row.
+template <bool OUT_F32, int N>
+__device__ __forceinline__ void store_row(void* out, int64_t off, const uint32_t (&o)[N], float scale) {
   if constexpr (OUT_F32) {
     float4* dst = reinterpret_cast<float4*>(static_cast<float*>(out) + off);
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < N / 4; ++i)
       dst[i] = make_float4(__uint_as_float(o[4 * i]) * scale, __uint_as_float(o[4 * i + 1]) * scale,
                            __uint_as_float(o[4 * i + 2]) * scale, __uint_as_float(o[4 * i + 3]) * scale);
   } else {
     uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + off);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < N / 8; ++i)
       dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * scale, __uint_as_float(o[8 * i + 1]) * scale),
                           pack_bf16(__uint_as_float(o[8 * i + 2]) * scale, __uint_as_float(o[8 * i + 3]) * scale),
                           pack_bf16(__uint_as_float(o[8 * i + 4]) * scale, __uint_as_float(o[8 * i + 5]) * scale),
                           pack_bf16(__uint_as_float(o[8 * i + 6]) * scale, __uint_as_float(o[8 * i + 7]) * scale));
   }
 }
+template <bool OUT_F32>
+__device__ __forceinline__ void store_row32(void* out, int64_t off, const uint32_t (&o)[32], float scale) {
+  store_row<OUT_F32, 32>(out, off, o, scale);
+}
 
 int launch_attn_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, int d, bool out_f32,
                    cudaStream_t stream);
+int launch_attn_exact(const CUtensorMap* maps, const void* q, const AttnParams& p, int d, bool out_f32,
+                      cudaStream_t stream);
 int launch_attn_sync(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
 
 }  // namespace fga

@@ -192,12 +192,14 @@ def test_unsorted_duplicate_free_lists_and_stride(d):
 
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("order", ["ascending", "descending"])
-def test_online_rescale_large_dynamic_range(d, order):
-    # scores grow by ~50 log2 units along the key list, so the running max moves many times
-    # (the kernel's lazy-rescale slow path) -- or, descending, never after the first chunk
+@pytest.mark.parametrize("gain", [4.0, 16.0])
+def test_online_rescale_large_dynamic_range(d, order, gain):
+    # Scores grow along the key list by ~50 (gain 4) or ~300 (gain 16) log2 units, so the
+    # running max moves many times (the kernel's lazy-rescale slow path) -- or, descending,
+    # never after the first chunk.
     b, h, n, m = 1, 2, 1536, 128
     rng = np.random.default_rng(11 + d)
-    q = oracle.bf16_round(4.0 * rng.standard_normal((b, h, n, d)).astype(np.float32))
+    q = oracle.bf16_round(gain * rng.standard_normal((b, h, n, d)).astype(np.float32))
     ramp = (0.2 + 3.0 * np.arange(n) / n).astype(np.float32)
     k = oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32) * ramp[None, None, :, None])
     v = oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32))
