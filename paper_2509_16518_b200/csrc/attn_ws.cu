@@ -48,11 +48,11 @@ namespace fga {
 namespace {
 
 constexpr int NSOFT = 8;        // softmax warps
-constexpr int WARP_S = 8;       // issuer of S = Q K^T
-constexpr int WARP_PV = 9;      // issuer of O += P V
+constexpr int WARP_MMA0 = 8;    // MMA issuers 8 (buffer 0) and 9 (buffer 1)
 constexpr int WARP_PROD0 = 10;
-constexpr int NPR = 3;          // producer warps per ring (K ring, V ring)
-constexpr int NWARPS = WARP_PROD0 + 2 * NPR;
+constexpr int NPK = 3;          // producer warps of the K ring = its slots (one warp per slot)
+constexpr int NPV = 3;          // producer warps of the V ring = its slots
+constexpr int NWARPS = 16;
 constexpr int REG_SOFTMAX = 184;
 constexpr int REG_OTHER = 72;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units (factor 256)
@@ -71,6 +71,9 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 #ifndef FGA_POLY_DEG
 #define FGA_POLY_DEG 3
 #endif
+#ifndef FGA_EXP_SKIP
+#define FGA_EXP_SKIP 0  // timing experiments only
+#endif
 #ifndef FGA_EXP_H2
 #define FGA_EXP_H2 0
 #endif
@@ -78,15 +81,20 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 template <int D>
 struct WsSmem {
   static constexpr int KV = (D / 64) * HALF;       // one K or V chunk
-  static constexpr int NSK = D == 128 ? 4 : 7;     // K ring slots
-  static constexpr int NSV = D == 128 ? 3 : 6;     // V ring slots
+  static constexpr int NSK = NPK;  // K ring slots
+  static constexpr int NSV = NPV;  // V ring slots
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + NSK * KV;
   static constexpr int OFF_BAR = OFF_V + NSV * KV;
   static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3;
   static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row
   static constexpr int BYTES = OFF_XCH + 2 * 128 * 4;
-  static_assert(NPR <= NSK && NPR <= NSV, "more producer warps than ring slots breaks the empty-barrier parity");
+  // The two issuers free a ring's slots in chunk order only up to swaps of neighbouring
+  // chunks (c and c+1 come from different issuers).  With one producer warp per slot a
+  // producer waits only for its own slot's previous use, which it issued itself after the
+  // use before had been freed, so the empty-barrier parity can never be two phases behind.
+  static_assert(NPK == NSK && NPV == NSV, "one producer warp per ring slot");
+  static_assert(WARP_PROD0 + NPK + NPV <= NWARPS, "too many producer warps");
 };
 
 struct Bars {
@@ -125,14 +133,14 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
 // ------------------------------------------------------------------ producers
 // Two rings, each filled and drained in chunk order: ring kv = 0 holds K chunks
 // (freed by the S issuer), ring kv = 1 holds V chunks (freed by the PV issuer).
-// Producer warp w of a ring packs the ring's chunks w, w+NPR, ... (CTA-wide
+// Producer warp w of a ring owns slot w and packs the ring's chunks w, w+npr, ... (CTA-wide
 // chunk order).  Each lane holds 4 of the chunk's 128 keys (loaded before the
 // slot wait); one warp instruction copies RPI rows (LPR lanes x 16 B per row).
 // Rows past the list end are zero-filled (src-size 0), so no stale or NaN bytes
-// reach the MMA.  NPR <= ring slots keeps the empty-barrier parity unambiguous.
+// reach the MMA.
 template <int D>
 __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
-                                         uint8_t* smem, const Bars& bar, int kv, int pw, int lane) {
+                                         uint8_t* smem, const Bars& bar, int kv, int pw, int npr, int lane) {
   using L = WsSmem<D>;
   constexpr int LPR = D / 8;     // lanes per 2*D-byte row
   constexpr int RPI = 32 / LPR;  // rows per warp instruction
@@ -151,7 +159,7 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
     const Tile t = decode_tile(p, tile);
     const uint32_t n = static_cast<uint32_t>(t.nchunks);
     const char* gsrc = static_cast<const char*>(kv ? p.v : p.k) + static_cast<int64_t>(t.row0) * (D * 2) + ch * 16;
-    for (uint32_t item = base + (static_cast<uint32_t>(pw) + NPR - base % NPR) % NPR; item < base + n; item += NPR) {
+    for (uint32_t item = base + (static_cast<uint32_t>(pw) + npr - base % npr) % npr; item < base + n; item += npr) {
       const int c = static_cast<int>(item - base);
       const uint32_t slot = item % nslot, use = item / nslot;
       uint64_t* full = &fullb[slot];
@@ -217,94 +225,83 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
 }
 
 // ------------------------------------------------------------------ MMA issuers
-// Two warps feed the tensor core so one's barrier waits overlap the other's
-// issue (a tcgen05.mma issue stalls until the MMA unit takes it, so a single
-// issuer leaves the unit idle across every wait).  In each warp the loop is
-// warp-uniform and one elected lane issues.  Ordering between them is by
-// completion barriers only: S_c reuses the TMEM buffer whose P_{c-2} feeds
-// PV_{c-2}, so the S issuer waits for PV_{c-2} to complete (pv_done).
+// Two issuer warps, one per S/P buffer: issuer r owns the chunks of CTA-wide parity r
+// and issues, for each of them in order, S_c = Q K_c^T into S[r] and then (after the
+// softmax) O += P_c V_c.  S_{c+2} reuses the buffer PV_c reads, and both come from the
+// same thread, so tcgen05's in-order execution is all the ordering needed: no
+// completion wait sits between PV_c and S_{c+2}.  Two issuers matter because a
+// tcgen05.mma issue stalls until the MMA unit takes it: while one chain waits for its
+// softmax, the other keeps the tensor core fed.  O starts each tile at zero (the
+// epilogue clears it), so every PV accumulates and the two chains' PVs commute.
 template <int D>
-__device__ __forceinline__ void s_issuer(const AttnParams& p, uint8_t* smem, const Bars& bar, uint32_t tmem) {
+__device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, const Bars& bar, uint32_t tmem, int r) {
   using L = WsSmem<D>;
   constexpr uint32_t IDESC_S = idesc_bf16(BM, BN, false, false);  // Q (TMEM), K K-major
+  constexpr uint32_t IDESC_O = idesc_bf16(BM, D, false, true);    // P (TMEM), V MN-major
   const uint64_t dk0 = sdesc_sw128(smem_u32(smem + L::OFF_K), 16, 1024);
-  const uint32_t tQ = tmem + TM_Q;
-  uint32_t c = 0, slot = 0, use = 0;  // CTA-wide chunk counter, K ring position
-  int it = 0;
-  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
-    const Tile t = decode_tile(p, tile);
-    if (t.nchunks > 0) {
-      mbar_wait(bar.q_full, it & 1);
-      FGA_TT(p, it, 1);
-    }
-    for (int j = 0; j < t.nchunks; ++j, ++c) {
-      FGA_TS(p, it, j, 8);
-      if (c >= 2) mbar_wait(&bar.pv_done[c & 1], ((c - 2) >> 1) & 1);  // S[c&1] free (PV_{c-2} done)
-      mbar_wait(&bar.k_full[slot], use & 1);
-      FGA_TS(p, it, j, 9);
-      fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
-      tc_fence_after();
-      const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
-      const uint32_t tS = tmem + TM_S + (c & 1) * 128;
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
-          umma_ts(tS, tQ + kk * 8, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(&bar.s_full[c & 1]);
-        umma_commit(&bar.k_empty[slot]);
-      }
-      __syncwarp();
-      FGA_TS(p, it, j, 14);
-      if (++slot == L::NSK) {
-        slot = 0;
-        ++use;
-      }
-    }
-  }
-}
-
-template <int D>
-__device__ __forceinline__ void pv_issuer(const AttnParams& p, uint8_t* smem, const Bars& bar, uint32_t tmem) {
-  using L = WsSmem<D>;
-  constexpr uint32_t IDESC_O = idesc_bf16(BM, D, false, true);  // P (TMEM), V MN-major
   const uint64_t dv0 = sdesc_sw128(smem_u32(smem + L::OFF_V), HALF, 1024);
-  const uint32_t tO = tmem + TM_O;
-  uint32_t c = 0, slot = 0, use = 0;
+  const uint32_t tQ = tmem + TM_Q, tO = tmem + TM_O, tS = tmem + TM_S + r * 128;
+  uint32_t c0 = 0;  // CTA-wide index of the tile's first chunk
   int it = 0;
   for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
-    for (int j = 0; j < t.nchunks; ++j, ++c) {
-      if (j == 0) {
-        mbar_wait(bar.o_empty, (it & 1) ^ 1);  // previous tile's epilogue has read O
-        FGA_TT(p, it, 2);
-      }
-      FGA_TS(p, it, j, 10);
-      mbar_wait(&bar.p_full[c & 1], (c >> 1) & 1);
-      FGA_TS(p, it, j, 11);
-      mbar_wait(&bar.v_full[slot], use & 1);
-      fence_proxy_async_smem();
-      tc_fence_after();
-      const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
-      const uint32_t tP = tmem + TM_S + (c & 1) * 128;
-      if (elect_one()) {
+    mbar_wait(bar.q_full, it & 1);  // waited every tile, so the phase never runs two ahead
+    if (r == 0) FGA_TT(p, it, 1);
+    tc_fence_after();
+    bool o_free = false;
+    for (int j = (r - static_cast<int>(c0 & 1)) & 1; j < t.nchunks; j += 2) {
+      const uint32_t c = c0 + j;
+      // ---- S_c = Q K_c^T
+      {
+        const uint32_t slot = c % L::NSK, use = c / L::NSK;
+        if (r == 0) FGA_TS(p, it, j, 8);
+        mbar_wait(&bar.k_full[slot], use & 1);
+        if (r == 0) FGA_TS(p, it, j, 9);
+        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
+        tc_fence_after();
+        const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
-          umma_ts(tO, tP + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&bar.v_empty[slot]);
-        umma_commit(&bar.pv_done[c & 1]);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
+            umma_ts(tS, tQ + kk * 8, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&bar.s_full[r]);
+          umma_commit(&bar.k_empty[slot]);
+        }
+        __syncwarp();
+        if (r == 0) FGA_TS(p, it, j, 14);
       }
-      __syncwarp();
-      FGA_TS(p, it, j, 12);
-      if (++slot == L::NSV) {
-        slot = 0;
-        ++use;
+      // ---- O += P_c V_c
+      {
+        if (!o_free) {
+          mbar_wait(bar.o_empty, it & 1);  // O cleared by the previous tile's epilogue
+          tc_fence_after();
+          o_free = true;
+        }
+        if (r == 0) FGA_TS(p, it, j, 10);
+        mbar_wait(&bar.p_full[r], (c >> 1) & 1);
+        if (r == 0) FGA_TS(p, it, j, 11);
+        const uint32_t slot = c % L::NSV, use = c / L::NSV;
+        mbar_wait(&bar.v_full[slot], use & 1);
+        fence_proxy_async_smem();
+        tc_fence_after();
+        const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) umma_ts(tO, tS + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, 1u);
+          umma_commit(&bar.v_empty[slot]);
+          umma_commit(&bar.pv_done[r]);
+        }
+        __syncwarp();
+        if (r == 0) FGA_TS(p, it, j, 12);
       }
     }
-    if (elect_one()) umma_commit(bar.o_full);
+    if (!o_free) mbar_wait(bar.o_empty, it & 1);  // keep the phase in step on a tile without our chunks
+    if (elect_one()) umma_commit(bar.o_full);      // count 2: both chains' PVs of this tile complete
     __syncwarp();
-    FGA_TT(p, it, 3);
+    if (r == 0) FGA_TT(p, it, 3);
+    c0 += t.nchunks;
   }
 }
 
@@ -356,7 +353,9 @@ __device__ __forceinline__ void exp_chunk(const uint32_t (&sv)[2][32], float sl2
         const float2 sx = make_float2(__uint_as_float(sv[hh][4 * k + 2 * r]), __uint_as_float(sv[hh][4 * k + 2 * r + 1]));
         const float2 x = __ffma2_rn(sx, sc2, nm[r]);
         float2 pr;
-        if (FGA_EXP_H2) {
+        if (FGA_EXP_SKIP > 0 && ((8 * hh + k) * 2 + r) % FGA_EXP_SKIP == 0) {
+          pr = x;  // timing experiment only: no exp for these pairs
+        } else if (FGA_EXP_H2) {
           pr = ex2_h2(x);
         } else if (((8 * hh + k) * 2 + r) % POLY_EVERY == POLY_EVERY - 1) {
           pr = ex2_poly2<FGA_POLY_DEG>(x);
@@ -382,13 +381,23 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
   const bool tr = tid == 0;
   uint32_t chunk = 0;
   int it = 0;
+  constexpr int NQ32 = D / 64;  // 32-column blocks of O per warp (rows 32q.., columns h*D/2..)
+  const uint32_t tOw = tmem + TM_O + (static_cast<uint32_t>(q * 32) << 16) + h * (D / 2);
+  uint32_t zero[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) zero[i] = 0u;
   int64_t tile = p.tile_begin + blockIdx.x;
   if (tile < p.n_tiles) {
     write_q<D>(p, qptr, decode_tile(p, tile), tmem, q, h, lane);
+#pragma unroll
+    for (int i = 0; i < NQ32; ++i) tmem_st32(tOw + i * 32, zero);  // every PV accumulates into O
     tmem_st_wait();
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(bar.q_full);
+    if (lane == 0) {
+      mbar_arrive(bar.q_full);
+      mbar_arrive(bar.o_empty);
+    }
   }
   for (; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
@@ -527,22 +536,19 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
     tc_fence_after();
     const bool valid = row < t.rows;
     const int64_t out_row = static_cast<int64_t>(t.row0) + t.q0 + row;
-    constexpr int NQ32 = D / 64;  // 32-column blocks per warp
     uint32_t o[NQ32][32];
 #pragma unroll
-    for (int i = 0; i < NQ32; ++i) tmem_ld32(tmem + TM_O + (static_cast<uint32_t>(q * 32) << 16) + h * (D / 2) + i * 32, o[i]);
+    for (int i = 0; i < NQ32; ++i) tmem_ld32(tOw + i * 32, o[i]);
     tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < NQ32; ++i) tmem_st32(tOw + i * 32, zero);  // cleared for the next tile
+    tmem_st_wait();
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(bar.o_empty);  // O is in registers: the next tile's PV may start
+    if (lane == 0) mbar_arrive(bar.o_empty);  // O is in registers and zero again: the next tile's PVs may start
 #pragma unroll
-    for (int i = 0; i < NQ32; ++i) {
-      if (t.nchunks == 0) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) o[i][e] = 0u;  // empty list: TMEM holds stale data
-      }
+    for (int i = 0; i < NQ32; ++i)
       if (valid) store_row32<OUT_F32>(p.out, out_row * D + h * (D / 2) + i * 32, o[i], inv);
-    }
     if (h == 0 && valid && p.lse != nullptr)
       p.lse[out_row] = lrow > 0.f ? mrow * 0.69314718055994531f + logf(lrow) : -INFINITY;
     if (tid == 0) FGA_TT(p, it, 5);
@@ -578,7 +584,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
       mbar_init(&bar.pv_done[i], 1);
     }
     mbar_init(bar.q_full, NSOFT);
-    mbar_init(bar.o_full, 1);
+    mbar_init(bar.o_full, 2);
     mbar_init(bar.o_empty, NSOFT);
     fence_barrier_init();
   }
@@ -603,13 +609,12 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     softmax<D, OUT_F32>(p, qptr, bar, tmem, tid, reinterpret_cast<float*>(smem + L::OFF_XCH));
   } else {
     setmaxnreg_dec<REG_OTHER>();
-    if (warp == WARP_S) {
-      s_issuer<D>(p, smem, bar, tmem);
-    } else if (warp == WARP_PV) {
-      pv_issuer<D>(p, smem, bar, tmem);
-    } else {
-      const int w = warp - WARP_PROD0;
-      producer<D>(p, &tmK2, &tmV2, smem, bar, w / NPR, w % NPR, lane);
+    if (warp < WARP_PROD0) {
+      mma_chain<D>(p, smem, bar, tmem, warp - WARP_MMA0);
+    } else if (warp < WARP_PROD0 + NPK) {
+      producer<D>(p, &tmK2, &tmV2, smem, bar, 0, warp - WARP_PROD0, NPK, lane);
+    } else if (warp < WARP_PROD0 + NPK + NPV) {
+      producer<D>(p, &tmK2, &tmV2, smem, bar, 1, warp - WARP_PROD0 - NPK, NPV, lane);
     }
   }
   tc_fence_before();

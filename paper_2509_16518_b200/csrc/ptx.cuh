@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 
 namespace fga {
@@ -46,7 +47,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > (1ll << 32)) __trap();
+    if (clock64() - t0 > (1ll << 32)) {
+#ifdef FGA_WATCHDOG_PRINT
+      if ((threadIdx.x & 31) == 0)
+        printf("fga watchdog: block %d warp %d barrier smem 0x%x parity %u\n", blockIdx.x, threadIdx.x / 32,
+               smem_u32(bar), parity);
+      const long long t1 = clock64();
+      while (clock64() - t1 < (1ll << 32)) {  // let the other stuck warps report too
+      }
+#endif
+      __trap();
+    }
   }
 }
 
