@@ -83,6 +83,18 @@ int fga_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx
                      int fill_sentinel, void* stream);
 
 /*
+ * FGM1 slice-mask files (paper_2509_16518_b200/io.py) decoded on the
+ * device: the host parses the header and the per-row list starts (the lengths are
+ * interleaved with the lists), uploads the u32 payload once, and this scatters it
+ * into the fga_compact output layout.
+ *   words  : int32 view of the payload after the 48-byte header.
+ *   starts : int64 [rows]; row r's list is words[starts[r] .. starts[r] + words[starts[r]-1]).
+ *   idx, counts, fill_sentinel : as fga_compact.
+ */
+int fga_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, int64_t n, int32_t* idx,
+                    int64_t idx_stride, int32_t* counts, int fill_sentinel, void* stream);
+
+/*
  * FG-Attn forward (K2 gather producer + K3 tcgen05 consumer).
  * Replaces sparse.py:111-156 (sparse_attention), whose numerics are the
  * online softmax of tiled.py:48-77; equals oracle.py:55-82

@@ -21,5 +21,7 @@ from .sparse import (DeviceIndexMask, PackedTile, SparseIndexMask, compact_keep,
                      gather_rows, import_padded, mask_density, mask_jaccard, masked_dense_attention, random_mask,
                      random_mask_device, sparse_attention)
 from .tiled import dense_attention, flash_attention
+from . import io  # noqa: E402  (FGT1 / FGM1 formats)
+from .stream import IterStreamConfig, generate_stream, run_cached_pipeline
 
 __version__ = "0.1.0"

@@ -36,6 +36,7 @@ _SIGS = {
     "fga_compact": ([_P, _P, _I64, _I64, _P, _I64, _P, _I, _P], _I),
     "fga_pack_bits": ([_P, _I64, _I64, _P, _P], _I),
     "fga_compact_bits": ([_P, _I64, _I64, _P, _I64, _P, _I, _P], _I),
+    "fga_fgm1_unpack": ([_P, _P, _I64, _I64, _P, _I64, _P, _I, _P], _I),
     "fga_sparse_attn_fwd": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _P], _I),
     "fga_sparse_attn_fwd_tiles": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _I64, _I64, _P], _I),
     "fga_dense_attn_fwd": ([_P, _P, _P, _P, _I, _P, FgaShape, _P], _I),

@@ -109,6 +109,13 @@ int fga_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx
   return launch_compact_bits(bits, rows, n, idx, idx_stride, counts, fill_sentinel, static_cast<cudaStream_t>(stream));
 }
 
+int fga_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, int64_t n, int32_t* idx,
+                    int64_t idx_stride, int32_t* counts, int fill_sentinel, void* stream) {
+  if (rows > 0 && (!words || !starts || !idx || !counts)) return fail(FGA_EINVAL, "null pointer");
+  return launch_fgm1_unpack(words, starts, rows, n, idx, idx_stride, counts, fill_sentinel,
+                            static_cast<cudaStream_t>(stream));
+}
+
 int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
                         const int32_t* counts, void* o, int o_dtype, float* lse, fga_shape shape, void* stream) {
   int rc = check_shape(shape);

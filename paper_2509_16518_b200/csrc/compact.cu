@@ -243,4 +243,31 @@ int launch_compact(const uint8_t* keep, const float* scores, int64_t rows, int64
   return check_launch("fga_compact_kernel");
 }
 
+// FGM1 mask payload (io.py) -> device index layout.  Row r's list
+// is words[starts[r] .. starts[r] + words[starts[r] - 1]); one CTA per row copies it
+// into idx[r, :len] (coalesced u32 loads / stores), writes counts[r] and optionally
+// the -1 tail.  HBM-bound: 4 B read + 4 B written per index.
+__global__ void fga_fgm1_unpack_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ starts, int64_t n,
+                                       int32_t* __restrict__ idx, int64_t idx_stride, int32_t* __restrict__ counts,
+                                       int fill) {
+  const int64_t r = blockIdx.x;
+  const int64_t s = starts[r];
+  const int len = words[s - 1];
+  int32_t* dst = idx + r * idx_stride;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) dst[i] = words[s + i];
+  if (fill)
+    for (int64_t i = len + threadIdx.x; i < n; i += blockDim.x) dst[i] = -1;
+  if (threadIdx.x == 0) counts[r] = len;
+}
+
+int launch_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, int64_t n, int32_t* idx,
+                       int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream) {
+  if (rows < 0 || n <= 0 || idx_stride < n) return fail(FGA_EINVAL, "fgm1_unpack: need rows >= 0, n > 0, idx_stride >= n");
+  if (rows == 0) return FGA_OK;
+  if (rows >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "fgm1_unpack: too many rows");
+  fga_fgm1_unpack_kernel<<<static_cast<unsigned>(rows), 256, 0, stream>>>(words, starts, n, idx, idx_stride, counts,
+                                                                           fill);
+  return check_launch("fga_fgm1_unpack_kernel");
+}
+
 }  // namespace fga

@@ -30,6 +30,8 @@ int launch_gather(const void* matrix, int64_t rows, int64_t d, const int32_t* in
 int launch_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bits, cudaStream_t stream);
 int launch_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx, int64_t idx_stride,
                         int32_t* counts, int fill, cudaStream_t stream);
+int launch_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, int64_t n, int32_t* idx,
+                       int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream);
 int launch_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t n, int32_t* idx,
                    int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream);
 
