@@ -13,8 +13,9 @@ include/fgattn.h).  There is no CPU fallback.
 
 from .core import (GATHER, PRECISIONS, STREAM, AttnConfig, AttnMap, AttnTensor, NumericError, ShapeError,
                    TileEvent, analysis_scores, ingest, make_rng, new_tensor, round_bf16)
-from .masks import (STRATEGIES, CachedMaskState, MaskBuilderConfig, build_mask, build_mask_avg_query,
-                    build_mask_cached, build_mask_cached_qk, cached_group_max, pooled_query_scores, refresh_policy)
+from .masks import (STRATEGIES, CachedMaskState, MaskBuilderConfig, block_sparsity, block_sparsity_qk, build_mask,
+                    build_mask_avg_query, build_mask_cached, build_mask_cached_qk, cached_group_max,
+                    pooled_query_scores, refresh_policy, slice_sparsity, slice_sparsity_qk)
 from .pipeline import pack_keep_bits, sparse_attention_host
 from .perfmodel import CostReport, count_flops, flop_speedup, synthetic_trace, trace_flops
 from .sparse import (DeviceIndexMask, PackedTile, SparseIndexMask, compact_keep, compact_keep_bits, export_padded, full_mask,

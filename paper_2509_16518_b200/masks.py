@@ -30,6 +30,7 @@ from .sparse import DeviceIndexMask, SparseIndexMask, compact_keep
 __all__ = [
     "STRATEGIES", "MaskBuilderConfig", "CachedMaskState", "refresh_policy", "build_mask_cached",
     "build_mask_cached_qk", "pooled_query_scores", "build_mask_avg_query", "build_mask", "cached_group_max",
+    "block_sparsity", "slice_sparsity", "block_sparsity_qk", "slice_sparsity_qk",
 ]
 
 STRATEGIES = ("cached_threshold", "avg_query_threshold", "avg_query_topk")
@@ -171,3 +172,63 @@ def build_mask(q, k, cfg: AttnConfig, builder: MaskBuilderConfig, device_result:
     if builder.strategy == "cached_threshold":
         return build_mask_cached_qk(q, k, cfg, builder.tau, device_result)
     return build_mask_avg_query(q, k, cfg, builder, device_result)
+
+
+# ------------------------------------------------------------------ sparsity analyzers (masks.py:153-184)
+# Table-2 style statistics on the GPU.  The map forms take an explicit [B,H,N,N] map like
+# the reference; the ``_qk`` forms compute the same numbers from Q and K with the fused
+# group-max kernel (fga_cached_group_max), so Wan-scale N -- where the N x N map cannot be
+# materialised on a CPU -- is analysable.
+
+def _map_group_max(map_, group: int, rnd: int):
+    t = torch()
+    m = as_device(getattr(map_, "data", map_), t.float32)
+    if m.dim() != 4 or m.shape[2] != m.shape[3]:
+        raise ShapeError(f"expected [B, H, N, N] map, got {tuple(m.shape)}")
+    b, h, n, _ = m.shape
+    g = -(-n // group)
+    gmax = t.empty((b, h, g, n), dtype=t.float32, device=m.device)
+    _lib.call("fga_group_max_map", ptr(m), b * h, n, group, rnd, ptr(gmax), stream_ptr())
+    return gmax
+
+
+def _tile_fraction(gmax, block: int, tau: float) -> float:
+    """Fraction of block x block tiles (rows already reduced to row-blocks in gmax) whose
+    max is below tau, averaged over (b, h); a partial edge tile counts over its real extent."""
+    t = torch()
+    b, h, g, n = gmax.shape
+    pad = (-n) % block
+    gm = t.nn.functional.pad(gmax, (0, pad), value=-1.0) if pad else gmax   # -1 < tau: ignored by max
+    tile_max = gm.reshape(b, h, g, -1, block).amax(dim=-1)
+    return float((tile_max < tau).float().mean(dim=(2, 3)).mean().item())
+
+
+def block_sparsity(map_, block: int, tau: float) -> float:
+    """Fraction of block x block score tiles with every entry below tau (masks.py:153-173)."""
+    n = int((getattr(map_, "data", map_)).shape[2])
+    if not 1 <= block <= n:
+        raise ValueError(f"block must be in [1, {n}]")
+    return _tile_fraction(_map_group_max(map_, block, 0), block, tau)
+
+
+def slice_sparsity(map_, cfg: AttnConfig, tau: float) -> float:
+    """Fraction of (group, key) M x 1 slices whose scores all fall below tau (masks.py:176-184)."""
+    dims = tuple((getattr(map_, "data", map_)).shape)
+    if dims != (cfg.batch, cfg.heads, cfg.seq_len, cfg.seq_len):
+        raise ShapeError(f"map dims {dims} do not match config")
+    gmax = _map_group_max(map_, cfg.group_size, _round(cfg))
+    return float((gmax < tau).float().mean().item())
+
+
+def block_sparsity_qk(q, k, cfg: AttnConfig, block: int, tau: float) -> float:
+    """block_sparsity(attention_map(q, k)) without the N x N map."""
+    if not 1 <= block <= cfg.seq_len:
+        raise ValueError(f"block must be in [1, {cfg.seq_len}]")
+    bcfg = AttnConfig(cfg.batch, cfg.heads, cfg.seq_len, cfg.head_dim, group_size=block, scale=cfg.scale,
+                      precision="full")
+    return _tile_fraction(cached_group_max(q, k, bcfg), block, tau)
+
+
+def slice_sparsity_qk(q, k, cfg: AttnConfig, tau: float) -> float:
+    """slice_sparsity(attention_map(q, k), cfg, tau) without the N x N map."""
+    return float((cached_group_max(q, k, cfg) < tau).float().mean().item())
