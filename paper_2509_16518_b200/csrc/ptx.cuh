@@ -108,8 +108,11 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
                : "memory");
 }
 // 16-byte cp.async (LDGSTS) without the zero-fill operand.
+#ifndef FGA_CPASYNC_HINT
+#define FGA_CPASYNC_HINT ".L2::128B"
+#endif
 __device__ __forceinline__ void cp_async16_full(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  asm volatile("cp.async.cg.shared.global" FGA_CPASYNC_HINT " [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 // Arrive (without incrementing the pending count) on an mbarrier once all of
 // this thread's prior cp.async copies have landed.
