@@ -62,6 +62,12 @@ constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
 #define FGA_POLY_EVERY (1 << 20)
 #endif
 constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the FMA pipe (MUFU relief)
+#ifndef FGA_SPLIT_ST
+#define FGA_SPLIT_ST 0
+#endif
+#ifndef FGA_PREFETCH_S
+#define FGA_PREFETCH_S 0
+#endif
 #ifndef FGA_NOGATHER
 #define FGA_NOGATHER 0  // timing experiments only
 #endif
@@ -338,8 +344,11 @@ __device__ __forceinline__ void write_q(const AttnParams& p, const void* qptr, c
 // P = 2^(s*scale*log2e - m) for this thread's 2 rows x 32 scores: packed FFMA2 for the
 // argument, MUFU ex2 for most pairs and the FMA-pipe polynomial for 1 in POLY_EVERY pairs,
 // packed FADD2 row sums, bf16 pairs in the 16x128b register order.
+// SPLIT_ST: each 64-column half of P is stored to TMEM as soon as it is packed, so the
+// first store's latency overlaps the second half's exps.
+template <bool SPLIT_ST>
 __device__ __forceinline__ void exp_chunk(const uint32_t (&sv)[2][32], float sl2, const float (&m_use)[2],
-                                          uint32_t (&pk)[32], float2 (&sum2)[2][2]) {
+                                          uint32_t (&pk)[32], float2 (&sum2)[2][2], uint32_t tS) {
   const float2 sc2 = make_float2(sl2, sl2);
   const float2 nm[2] = {make_float2(-m_use[0], -m_use[0]), make_float2(-m_use[1], -m_use[1])};
 #pragma unroll
@@ -366,6 +375,12 @@ __device__ __forceinline__ void exp_chunk(const uint32_t (&sv)[2][32], float sl2
         sum2[r][k & 1] = __fadd2_rn(sum2[r][k & 1], pr);
         pk[2 * (8 * hh + k) + r] = pack_bf16(pr.x, pr.y);
       }
+    }
+    if constexpr (SPLIT_ST) {
+      uint32_t ph[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) ph[i] = pk[16 * hh + i];
+      tmem_st16x128_x8(tS + 32 * hh, ph);
     }
   }
 }
@@ -402,16 +417,19 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
   for (; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
     float m_use[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};  // l_run: this thread's partial sums
+    uint32_t sv[2][32];  // [column half][4k + 2*row + e]: rows r0/r0+8, col 64*half + 8k + 2a + e
+    bool have_s = false;  // sv is already loading S_j (issued at the end of the previous chunk)
     for (int j = 0; j < t.nchunks; ++j) {
       const uint32_t c = chunk + j;
       const uint32_t tS = tmem + TM_S + (c & 1) * 128 + lanes16;
       if (tr) FGA_TS(p, it, j, 0);
-      mbar_wait(&bar.s_full[c & 1], (c >> 1) & 1);
-      if (tr) FGA_TS(p, it, j, 1);
-      tc_fence_after();
-      uint32_t sv[2][32];  // [column half][4k + 2*row + e]: rows r0/r0+8, col 64*half + 8k + 2a + e
-      tmem_ld16x256_x8(tS, sv[0]);
-      tmem_ld16x256_x8(tS + 64, sv[1]);
+      if (!have_s) {
+        mbar_wait(&bar.s_full[c & 1], (c >> 1) & 1);
+        if (tr) FGA_TS(p, it, j, 1);
+        tc_fence_after();
+        tmem_ld16x256_x8(tS, sv[0]);
+        tmem_ld16x256_x8(tS + 64, sv[1]);
+      }
       tmem_ld_wait();
       if (tr) FGA_TS(p, it, j, 2);
       const int nvalid = min(BN, t.count - j * BN);
@@ -442,7 +460,7 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
         sum2[0][0] = sum2[0][1] = sum2[1][0] = sum2[1][1] = make_float2(1.f, 1.f);
         if (j == 0) m_use[0] = m_use[1] = 0.f;
       } else if (!slow) {
-        exp_chunk(sv, sl2, m_use, pk, sum2);
+        exp_chunk<FGA_SPLIT_ST>(sv, sl2, m_use, pk, sum2, tS);
         const float2 u0 = __fadd2_rn(sum2[0][0], sum2[0][1]), u1 = __fadd2_rn(sum2[1][0], sum2[1][1]);
         const bool over = !(u0.x + u0.y <= RESCALE_SUM) || !(u1.x + u1.y <= RESCALE_SUM);
         slow = __any_sync(0xffffffffu, over);
@@ -473,10 +491,10 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
             rescale = true;
           }
         }
-        exp_chunk(sv, sl2, m_use, pk, sum2);
+        exp_chunk<FGA_SPLIT_ST>(sv, sl2, m_use, pk, sum2, tS);
       }
       if (tr) FGA_TS(p, it, j, 3);
-      tmem_st16x128_x16(tS, pk);
+      if (!FGA_SPLIT_ST) tmem_st16x128_x16(tS, pk);
       if (tr) FGA_TS(p, it, j, 4);
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
@@ -499,6 +517,17 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
             tmem_st16x256_x8(tmem + TM_O + lanes16 + hh * 64, o);
           }
         }
+      }
+      // Load S_{j+1} now if it is ready (it does not depend on P_j), after P_j's store has been
+      // issued, so its TMEM latency overlaps the store wait and the barrier traffic below.
+      have_s = false;
+      if (FGA_PREFETCH_S && j + 1 < t.nchunks &&
+          __all_sync(0xffffffffu, mbar_try_wait(&bar.s_full[(c + 1) & 1], ((c + 1) >> 1) & 1))) {
+        tc_fence_after();
+        const uint32_t tSn = tmem + TM_S + ((c + 1) & 1) * 128 + lanes16;
+        tmem_ld16x256_x8(tSn, sv[0]);
+        tmem_ld16x256_x8(tSn + 64, sv[1]);
+        have_s = true;
       }
       tmem_st_wait();
       tc_fence_before();
