@@ -100,7 +100,7 @@ class HostPipeline:
 _pipes: dict = {}
 
 
-def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: int = 4):
+def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: int = 6):
     """FG-Attn from pinned host buffers (see module doc).  Returns the pinned host output;
     synchronise the current stream before reading it."""
     t = torch()
