@@ -46,14 +46,22 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
   const int64_t span = head + n;
   const int64_t nblk = (span + 15) >> 4;
 
+  // the next round's 16-byte block is loaded before this round's scan (two loads in flight)
+  auto load = [&](int64_t blk) -> uint4 {
+    const int64_t lo = blk * 16;
+    return (blk < nblk && lo >= head && lo + 16 <= span) ? __ldg(reinterpret_cast<const uint4*>(abase + lo))
+                                                         : make_uint4(0u, 0u, 0u, 0u);
+  };
+  uint4 wn = load(tid);
   int running = 0;
   for (int64_t b0 = 0; b0 < nblk; b0 += T) {
     const int64_t blk = b0 + tid;
+    const uint4 w = wn;
+    wn = load(blk + T);
     uint32_t bits = 0;
     if (blk < nblk) {
       const int64_t lo = blk * 16;
       if (lo >= head && lo + 16 <= span) {
-        const uint4 w = __ldg(reinterpret_cast<const uint4*>(abase + lo));
         bits = nonzero_bytes(w.x) | (nonzero_bytes(w.y) << 4) | (nonzero_bytes(w.z) << 8) | (nonzero_bytes(w.w) << 12);
       } else {
 #pragma unroll 4
