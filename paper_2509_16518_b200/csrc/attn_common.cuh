@@ -37,7 +37,8 @@ struct AttnParams {
 #define FGA_TRACE_SLOTS 16
 #define FGA_TRACE_TILE_OFF (64 * FGA_TRACE_SLOTS)
 #define FGA_TRACE_CTA_OFF (FGA_TRACE_TILE_OFF + 32 * 8)
-#define FGA_TRACE_LEN (FGA_TRACE_CTA_OFF + 2 * 1024)
+#define FGA_TRACE_WARP_OFF (FGA_TRACE_CTA_OFF + 2 * 1024)  // per softmax warp: p_full arrive of chunk j < 64
+#define FGA_TRACE_LEN (FGA_TRACE_WARP_OFF + 64 * 16)
 #ifndef FGA_TRACE_ON
 #define FGA_TRACE_ON 0  // timeline hooks are compiled in only for the trace build (scripts/trace_run.py)
 #endif
@@ -52,7 +53,15 @@ struct AttnParams {
     if ((p).trace != nullptr && blockIdx.x == 0 && (it) < 32)                                           \
       (p).trace[FGA_TRACE_TILE_OFF + (it) * 8 + (slot)] = clock64();                                    \
   } while (0)
+#define FGA_TW(p, it, j, w)                                                                            \
+  do {                                                                                                  \
+    if ((p).trace != nullptr && blockIdx.x == 0 && (it) == (p).trace_it && (j) < 64)                    \
+      (p).trace[FGA_TRACE_WARP_OFF + (j) * 16 + (w)] = clock64();                                       \
+  } while (0)
 #else
+#define FGA_TW(p, it, j, w) \
+  do {                      \
+  } while (0)
 #define FGA_TS(p, it, j, slot) \
   do {                         \
   } while (0)

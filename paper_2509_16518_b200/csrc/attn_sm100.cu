@@ -341,6 +341,10 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
       }
       for (int b = 0; b < 1024; ++b)
         std::fprintf(f, "%lld %lld\n", host[FGA_TRACE_CTA_OFF + 2 * b], host[FGA_TRACE_CTA_OFF + 2 * b + 1]);
+      for (int j = 0; j < 64; ++j) {
+        for (int w = 0; w < 16; ++w) std::fprintf(f, "%lld ", host[FGA_TRACE_WARP_OFF + j * 16 + w]);
+        std::fprintf(f, "\n");
+      }
       std::fclose(f);
     }
     return rc2;

@@ -534,6 +534,7 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar.p_full[c & 1]);
       if (tr) FGA_TS(p, it, j, 5);
+      if (lane == 0) FGA_TW(p, it, j, warp);
     }
     chunk += t.nchunks;
     // every S of this tile has been consumed, so Q may be replaced by the next tile's

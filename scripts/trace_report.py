@@ -6,7 +6,9 @@ import numpy as np
 lines = open(sys.argv[1]).read().split("\n")
 t = np.array([[int(x) for x in l.split()] for l in lines[:64]], dtype=np.int64)
 tt = np.array([[int(x) for x in l.split()] for l in lines[64:96]], dtype=np.int64)
-cta = np.array([[int(x) for x in l.split()] for l in lines[96:] if l.strip()], dtype=np.int64)
+cta = np.array([[int(x) for x in l.split()] for l in lines[96:96 + 1024] if l.strip()], dtype=np.int64)
+wl = [l for l in lines[96 + 1024:96 + 1024 + 64] if l.strip()]
+warp_arrive = np.array([[int(x) for x in l.split()] for l in wl], dtype=np.int64) if wl else None
 mm = t[:, 8] > 0
 j = np.nonzero(mm)[0]
 r = j[(j >= 4) & (j < j.max() - 2)]
@@ -33,3 +35,8 @@ if len(c):
     d = (c[:, 1] - c[:, 0]) / 1e3
     print(f"CTAs {len(c)}: start spread {(c[:, 0].max() - t0) / 1e3:.1f} us, duration min {d.min():.1f} "
           f"median {np.median(d):.1f} max {d.max():.1f} us, end spread {(c[:, 1].max() - c[:, 1].min()) / 1e3:.1f} us")
+
+if warp_arrive is not None and (warp_arrive[:, :8] > 0).all(axis=1).any():
+    rows = [r for r in range(4, len(warp_arrive) - 2) if (warp_arrive[r, :8] > 0).all()]
+    lag = np.array([warp_arrive[r, :8] - warp_arrive[r, :8].min() for r in rows])
+    print(" softmax warp arrive lag behind the first warp (cycles), per warp 0..7:", lag.mean(0).round(0).tolist())
