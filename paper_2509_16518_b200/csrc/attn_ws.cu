@@ -65,6 +65,15 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 #ifndef FGA_SPLIT_ST
 #define FGA_SPLIT_ST 0
 #endif
+#ifndef FGA_TMA_GATHER
+#define FGA_TMA_GATHER 0  // bit 0: K rows, bit 1: V rows by TMA tile::gather4 (else 16-byte cp.async)
+#endif
+#ifndef FGA_PROD_SPLIT
+#define FGA_PROD_SPLIT 1  // 1: four producer warps, one per sub-partition, half a chunk each
+#endif
+#ifndef FGA_PROD_SWAP
+#define FGA_PROD_SWAP 0  // FGA_PROD_SPLIT: 1 puts the V halves on sub-partitions 2, 3 and K on 0, 1
+#endif
 #ifndef FGA_PREFETCH_S
 #define FGA_PREFETCH_S 0
 #endif
@@ -146,7 +155,8 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
 // reach the MMA.
 template <int D>
 __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
-                                         uint8_t* smem, const Bars& bar, int kv, int pw, int npr, int lane) {
+                                         const CUtensorMap* tmKg, const CUtensorMap* tmVg, uint8_t* smem,
+                                         const Bars& bar, int kv, int pw, int npr, int lane) {
   using L = WsSmem<D>;
   constexpr int LPR = D / 8;     // lanes per 2*D-byte row
   constexpr int RPI = 32 / LPR;  // rows per warp instruction
@@ -160,6 +170,7 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
   uint64_t* fullb = kv ? bar.v_full : bar.k_full;
   uint64_t* emptyb = kv ? bar.v_empty : bar.k_empty;
   const CUtensorMap* tm = kv ? tmV2 : tmK2;
+  const CUtensorMap* tmg = kv ? tmVg : tmKg;
   uint32_t base = 0;  // CTA-wide index of the tile's first chunk
   for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
     const Tile t = decode_tile(p, tile);
@@ -179,6 +190,26 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
         } else {
           mbar_arrive(full);
         }
+        continue;
+      }
+      if (FGA_TMA_GATHER & (1 << kv)) {
+        // TMA tile::gather4: lane l gathers rows 4l..4l+3 of the chunk (both 64-column halves);
+        // rows past the list end repeat the chunk's first key (their scores are masked to -inf,
+        // so their P is 0 and the repeated V row contributes nothing).  The copy engine does
+        // the swizzle, and the SM sub-partition issues 2 instructions per chunk instead of 64
+        // LDGSTS, which would otherwise share the MIO queue with the softmax's MUFU.EX2.
+        const int r0 = c * BN + 4 * lane;
+        const int first = __ldg(t.list + c * BN);
+        int rk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) rk[e] = t.row0 + (r0 + e < t.count ? __ldg(t.list + r0 + e) : first);
+        mbar_wait(&emptyb[slot], (use & 1) ^ 1);
+        if (lane == 0) mbar_expect_tx(full, BN * D * 2);
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < D / 64; ++h)
+          tma_gather4(ring + slot * L::KV + h * HALF + 4 * lane * 128, tmg, full, h * 64, rk[0], rk[1], rk[2], rk[3],
+                      pol_kv);
         continue;
       }
       int keys[4];
@@ -227,6 +258,87 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
       cp_async_arrive_noinc(full);
     }
     base += n;
+  }
+}
+
+// Balanced producers (FGA_PROD_SPLIT): four warps, one per SM sub-partition, each packing
+// one 64-row half of every chunk of one ring (warp 10: K rows 0-63, 11: K rows 64-127,
+// 12: V rows 0-63, 13: V rows 64-127 -> sub-partitions 2, 3, 0, 1).  The LDGSTS traffic,
+// which queues with the softmax's MUFU.EX2 in each sub-partition's MIO unit, is then the
+// same in every TMEM lane quadrant.  A slot completes with both halves' 64 arrivals, so
+// each warp sees every use of every slot of its ring and the empty parity stays exact.
+template <int D>
+__device__ __forceinline__ void producer_half(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
+                                              uint8_t* smem, const Bars& bar, int kv, int part, int lane) {
+  using L = WsSmem<D>;
+  constexpr int LPR = D / 8;     // lanes per 2*D-byte row
+  constexpr int RPI = 32 / LPR;  // rows per warp instruction
+  constexpr int ROWS = BN / 2;
+  const int nslot = kv ? L::NSV : L::NSK;
+  const uint64_t pol_kv = policy_evict_last();
+  const int sub = lane / LPR, ch = lane % LPR;
+  const uint32_t lane_off = static_cast<uint32_t>((ch >> 3) * HALF);
+  const int cc = ch & 7;
+  uint8_t* ring = smem + (kv ? L::OFF_V : L::OFF_K);
+  const uint32_t ring_base = smem_u32(ring) + part * ROWS * 128;
+  uint64_t* fullb = kv ? bar.v_full : bar.k_full;
+  uint64_t* emptyb = kv ? bar.v_empty : bar.k_empty;
+  const CUtensorMap* tm = kv ? tmV2 : tmK2;
+  constexpr int PER = 8 / RPI;
+  uint32_t item = 0;
+  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    const Tile t = decode_tile(p, tile);
+    const char* gsrc = static_cast<const char*>(kv ? p.v : p.k) + static_cast<int64_t>(t.row0) * (D * 2) + ch * 16;
+    for (int c = 0; c < t.nchunks; ++c, ++item) {
+      const uint32_t slot = item % nslot, use = item / nslot;
+      uint64_t* full = &fullb[slot];
+      if (p.dense) {
+        mbar_wait(&emptyb[slot], (use & 1) ^ 1);
+        if (part == 0 && lane == 0) {
+          mbar_expect_tx(full, BN * D * 2);
+#pragma unroll
+          for (int h = 0; h < D / 64; ++h)
+            tma_load_2d(ring + slot * L::KV + h * HALF, tm, full, h * 64, t.row0 + c * BN, pol_kv);
+        } else {
+          mbar_arrive(full);
+        }
+        continue;
+      }
+      int keys[ROWS / 32];
+#pragma unroll
+      for (int i = 0; i < ROWS / 32; ++i) {
+        const int row = c * BN + part * ROWS + i * 32 + lane;
+        keys[i] = row < t.count ? __ldg(t.list + row) : -1;
+      }
+      mbar_wait(&emptyb[slot], (use & 1) ^ 1);
+      const char* src = gsrc;
+      asm volatile("mov.b64 %0, %0;" : "+l"(src));
+      uint32_t dstb[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u)
+        dstb[u] = ring_base + slot * L::KV + lane_off + sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
+      if (c * BN + part * ROWS + ROWS <= t.count) {
+#pragma unroll
+        for (int i = 0; i < ROWS / 32; ++i) {
+#pragma unroll
+          for (int mm = 0; mm < 32 / RPI; ++mm) {
+            const uint32_t key = static_cast<uint32_t>(__shfl_sync(0xffffffffu, keys[i], mm * RPI + sub));
+            cp_async16_full(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, src + static_cast<size_t>(key) * (D * 2));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < ROWS / 32; ++i) {
+#pragma unroll
+          for (int mm = 0; mm < 32 / RPI; ++mm) {
+            const int key = __shfl_sync(0xffffffffu, keys[i], mm * RPI + sub);
+            const char* g = src + static_cast<size_t>(static_cast<uint32_t>(max(key, 0))) * (D * 2);
+            cp_async16(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, g, key >= 0 ? 16u : 0u);
+          }
+        }
+      }
+      cp_async_arrive_noinc(full);
+    }
   }
 }
 
@@ -588,6 +700,7 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
 template <int D, bool OUT_F32>
 __global__ void __launch_bounds__(32 * NWARPS, 1)
     fga_attn_ws_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_constant__ CUtensorMap tmV2,
+                       const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
                        const void* __restrict__ qptr, const AttnParams p) {
   using L = WsSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_ws[];
@@ -599,13 +712,20 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     if (p.dense) {
       prefetch_tmap(&tmK2);
       prefetch_tmap(&tmV2);
+    } else if (FGA_TMA_GATHER != 0) {
+      prefetch_tmap(&tmKg);
+      prefetch_tmap(&tmVg);
     }
+    // a chunk completes with 32 cp.async arrivals (LDGSTS producer, dense path: lane 0's
+    // expect_tx + 31 arrivals) or with lane 0's expect_tx alone (gather4 producer)
+    const uint32_t k_count = FGA_PROD_SPLIT ? 64u : ((FGA_TMA_GATHER & 1) && !p.dense) ? 1u : 32u;
+    const uint32_t v_count = FGA_PROD_SPLIT ? 64u : ((FGA_TMA_GATHER & 2) && !p.dense) ? 1u : 32u;
     for (int i = 0; i < L::NSK; ++i) {
-      mbar_init(&bar.k_full[i], 32);  // one producer warp per chunk
+      mbar_init(&bar.k_full[i], k_count);  // one producer warp per chunk
       mbar_init(&bar.k_empty[i], 1);
     }
     for (int i = 0; i < L::NSV; ++i) {
-      mbar_init(&bar.v_full[i], 32);
+      mbar_init(&bar.v_full[i], v_count);
       mbar_init(&bar.v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -641,10 +761,13 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     setmaxnreg_dec<REG_OTHER>();
     if (warp < WARP_PROD0) {
       mma_chain<D>(p, smem, bar, tmem, warp - WARP_MMA0);
+    } else if (FGA_PROD_SPLIT) {
+      if (warp < WARP_PROD0 + 4)
+        producer_half<D>(p, &tmK2, &tmV2, smem, bar, ((warp - WARP_PROD0) >> 1) ^ FGA_PROD_SWAP, (warp - WARP_PROD0) & 1, lane);
     } else if (warp < WARP_PROD0 + NPK) {
-      producer<D>(p, &tmK2, &tmV2, smem, bar, 0, warp - WARP_PROD0, NPK, lane);
+      producer<D>(p, &tmK2, &tmV2, &tmKg, &tmVg, smem, bar, 0, warp - WARP_PROD0, NPK, lane);
     } else if (warp < WARP_PROD0 + NPK + NPV) {
-      producer<D>(p, &tmK2, &tmV2, smem, bar, 1, warp - WARP_PROD0 - NPK, NPV, lane);
+      producer<D>(p, &tmK2, &tmV2, &tmKg, &tmVg, smem, bar, 1, warp - WARP_PROD0 - NPK, NPV, lane);
     }
   }
   tc_fence_before();
@@ -667,7 +790,7 @@ int launch_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, cudaS
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t span = p.n_tiles - p.tile_begin;
   const int64_t grid = span < sms ? span : sms;
-  kern<<<static_cast<unsigned>(grid), 32 * NWARPS, smem, stream>>>(maps[3], maps[4], q, p);
+  kern<<<static_cast<unsigned>(grid), 32 * NWARPS, smem, stream>>>(maps[3], maps[4], maps[1], maps[2], q, p);
   return check_launch("fga_attn_ws_kernel");
 }
 

@@ -202,10 +202,9 @@ int main(int argc, char** argv) {
       {5, 4, 1, "BOX  dense 128-row box"}, {5, 6, 2, "BOX  dense, 2 warps"},
       {0, 4, 8, "CP   coop"},  {0, 5, 11, "CP   coop"}, {0, 5, 15, "CP   coop"}, {0, 6, 16, "CP   coop"},
       {0, 6, 20, "CP   coop"}, {0, 6, 24, "CP   coop"},
-      {1, 4, 4, "CPW  warp/item"}, {1, 6, 6, "CPW  warp/item"}, {1, 6, 12, "CPW  warp/item"},
-      {1, 6, 24, "CPW  warp/item"},
+      {1, 4, 4, "CPW  warp/item"}, {1, 6, 6, "CPW  warp/item"}, {1, 3, 3, "CPW  warp/item"},
       {2, 4, 1, "G4W  gather4 warp/item"}, {2, 4, 2, "G4W  gather4 warp/item"}, {2, 6, 3, "G4W  gather4 warp/item"},
-      {2, 6, 6, "G4W  gather4 warp/item"},
+      {2, 6, 6, "G4W  gather4 warp/item"}, {2, 3, 3, "G4W  gather4 warp/item"},
       {6, 6, 6, "G4S  gather4 8 lanes"},
       {3, 4, 2, "ROW  tma box 1 row"}, {3, 6, 6, "ROW  tma box 1 row"},
       {4, 4, 2, "BULK 1D 256B/row"}, {4, 6, 6, "BULK 1D 256B/row"},
