@@ -325,6 +325,8 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
   if (p.trace != nullptr) {
     int rc2 = (which != nullptr && std::strcmp(which, "sync") == 0)
                   ? launch_attn_sync(maps, p, static_cast<int>(D), f32, stream)
+              : (which != nullptr && std::strcmp(which, "pp") == 0)
+                  ? launch_attn_pp(maps, p, static_cast<int>(D), f32, stream)
                   : launch_attn_ws(maps, q, p, static_cast<int>(D), f32, stream);
     static long long host[FGA_TRACE_LEN];
     cudaMemcpyAsync(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost, stream);
@@ -350,6 +352,7 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
     return rc2;
   }
   if (which != nullptr && std::strcmp(which, "sync") == 0) return launch_attn_sync(maps, p, static_cast<int>(D), f32, stream);
+  if (which != nullptr && std::strcmp(which, "pp") == 0) return launch_attn_pp(maps, p, static_cast<int>(D), f32, stream);
   return launch_attn_ws(maps, q, p, static_cast<int>(D), f32, stream);
 }
 
