@@ -253,6 +253,9 @@ class ClockSampler:
                 "samples": len(s)}
 
 
+GATHER_CEILING_GBS = 12214.0  # L2 -> SMEM, random 2*D-byte rows (profiles/r01/gather_bench2.log)
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -354,6 +357,7 @@ def ours(args):
 
     peak, peak_sus, hbm_peak, peak_src = measured_peaks()
     achieved = flops / (kernel_ms * 1e-3) / 1e12
+    gathered = int(rep.density * cfg.batch * heads * cfg.num_groups * n) * 4 * d  # K + V rows, bf16
     value = achieved * world
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -369,8 +373,13 @@ def ours(args):
                      "frac": achieved / peak, "frac_of_sustained": achieved / peak_sus if peak_sus else None,
                      "peak_source": peak_src, "traffic": ncu_traffic(args.config, args.density),
                      "algorithmic_flops_per_launch": flops,
-                     "gathered_kv_bytes_per_launch": int(rep.density * cfg.batch * heads * cfg.num_groups * n) * 4 * d,
-                     "kernel": "fga_attn_ws_kernel"},
+                     "gathered_kv_bytes_per_launch": gathered,
+                     "kernel": "fga_attn_ws_kernel",
+                     # the gathered K/V rows move L2 -> SMEM; their ceiling is the measured random-row
+                     # gather rate (scripts/gather_bench2.cu, profiles/r01/gather_bench2.log)
+                     "gather": {"achieved_gbs": gathered / (kernel_ms * 1e-3) / 1e9, "ceiling_gbs": GATHER_CEILING_GBS,
+                                "frac": gathered / (kernel_ms * 1e-3) / 1e9 / GATHER_CEILING_GBS,
+                                "ceiling_source": "measured: cp.async warp-per-chunk gather of random 256-byte rows"}},
         "clocks": clk.summary(),
         "wall_s_timed_region": wall,
     }
