@@ -1,4 +1,4 @@
-// FG-Attn forward on sm_100a: warp-specialised persistent kernel (v6).
+// FG-Attn forward on sm_100a: warp-specialised persistent kernel (v9).
 //
 // Reference semantics: /root/reference/pkg/src/sliceattn/sparse.py:111-156
 // (per-(b,h,g) chunk loop over the key list) with the online softmax of
@@ -6,13 +6,13 @@
 // is consumed in chunks of 128 gathered keys (a short last chunk is zero-filled
 // past the list end and its extra score columns are set to -inf).
 //
-// Per chunk j (issue order S_0, S_1, PV_0, S_2, PV_1, ...):
+// Per chunk j:
 //   S_j  = Q K_j^T   tcgen05 TS-MMA: Q (bf16) resident in TMEM, K_j from SMEM
 //   P_j  = 2^(S_j * scale * log2e - m)   softmax warps, written over S_j in TMEM
 //   O   += P_j V_j   tcgen05 TS-MMA: P_j from TMEM, V_j from SMEM
 // With Q in TMEM the tensor core reads only the gathered K and V from SMEM
 // (64 KB per chunk instead of 96 KB), which leaves SMEM bandwidth for the
-// gather's 64 KB of writes, and all 224 KB of SMEM for the K/V ring.
+// gather's 64 KB of writes, and all 224 KB of SMEM for the K/V rings.
 //
 // Softmax: 8 warps, two per TMEM lane quadrant.  Warp w owns the 16 query rows
 // 32(w%4) + 16(w/4) .. +15 (tcgen05 16x256b / 16x128b shapes: each thread holds
@@ -22,15 +22,11 @@
 //
 // Warps (16, one CTA per SM, persistent over tiles strided by the grid):
 //   0-7   softmax + epilogue (+ writing the next tile's Q into TMEM)
-//   8     MMA issuer (one warp, elected lane)
-//   9-15  item producers.  Every 128-key K or V chunk is one ring item, items in
-//         the order the MMA consumes them (K0, K1, V0, K2, V1, ...), item i
-//         packed entirely by producer i % 7 with 16-byte cp.async into a
-//         128B-swizzled slot.  One warp per item keeps items in flight
-//         independently; measured on B200 (scripts/gather_bench2.cu) this moves
-//         12.2 TB/s of random 256-byte rows L2->SMEM, against 7.5-8.3 TB/s when
-//         all producer warps cooperate on each item and 2.1 TB/s for TMA
-//         tile::gather4.
+//   8, 9  MMA issuers, one per S/P buffer (chunks of CTA-wide parity 0 / 1)
+//   10-13 gather producers (FGA_PROD_SPLIT, default): K rows 0-63, K rows 64-127,
+//         V rows 0-63, V rows 64-127 of every chunk, one warp per SM sub-partition,
+//         16-byte cp.async into the 128B-swizzled ring slots (3 K + 3 V)
+//   14, 15 idle (FGA_PROD_SPLIT=0: 10-15 are one producer warp per ring slot)
 // TMEM (512 cols): O [0, D) | Q [128, 128 + D/2) | S0 [256, 384) | S1 [384, 512).
 // P_j (bf16 pairs) overwrites S[j%2] cols 0..63.
 // Lazy rescale: the running max used for exp only moves when the row max grows
