@@ -67,6 +67,12 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 #ifndef FGA_PROD_SPLIT
 #define FGA_PROD_SPLIT 1  // 1: four producer warps, one per sub-partition, half a chunk each
 #endif
+#ifndef FGA_NSK
+#define FGA_NSK 3  // K ring slots (FGA_PROD_SPLIT)
+#endif
+#ifndef FGA_NSV
+#define FGA_NSV 3  // V ring slots (FGA_PROD_SPLIT)
+#endif
 #ifndef FGA_PROD_SWAP
 #define FGA_PROD_SWAP 0  // FGA_PROD_SPLIT: 1 puts the V halves on sub-partitions 2, 3 and K on 0, 1
 #endif
@@ -92,8 +98,9 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 template <int D>
 struct WsSmem {
   static constexpr int KV = (D / 64) * HALF;       // one K or V chunk
-  static constexpr int NSK = NPK;  // K ring slots
-  static constexpr int NSV = NPV;  // V ring slots
+  // K / V ring slots: one per producer warp (FGA_PROD_SPLIT=0), or any count up to what SMEM holds
+  static constexpr int NSK = FGA_PROD_SPLIT ? FGA_NSK : NPK;
+  static constexpr int NSV = FGA_PROD_SPLIT ? FGA_NSV : NPV;
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + NSK * KV;
   static constexpr int OFF_BAR = OFF_V + NSV * KV;
@@ -104,7 +111,8 @@ struct WsSmem {
   // chunks (c and c+1 come from different issuers).  With one producer warp per slot a
   // producer waits only for its own slot's previous use, which it issued itself after the
   // use before had been freed, so the empty-barrier parity can never be two phases behind.
-  static_assert(NPK == NSK && NPV == NSV, "one producer warp per ring slot");
+  static_assert(FGA_PROD_SPLIT || (NPK == NSK && NPV == NSV), "one producer warp per ring slot");
+  static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
   static_assert(WARP_PROD0 + NPK + NPV <= NWARPS, "too many producer warps");
 };
 

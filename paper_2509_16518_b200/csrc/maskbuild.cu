@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -376,6 +377,13 @@ int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, in
                             cudaStream_t st) {
   const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
   const int64_t G = (N + M - 1) / M;
+  // tensor-core passes for M = 128, D in {64, 128} (maskbuild_tc.cu); FGA_CACHED_CC=1 forces this file's
+  // CUDA-core passes (kept for other shapes and as a cross-check)
+  const char* cc = std::getenv("FGA_CACHED_CC");
+  if (cc == nullptr || cc[0] != '1') {
+    const int rc = launch_cached_group_max_tc(q, k, s, round, gmax, ws, st);
+    if (rc != FGA_EUNSUPPORTED) return rc;
+  }
   if (D % DK != 0) return fail(FGA_EUNSUPPORTED, "cached_group_max: head_dim must be a multiple of 32");
   const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
   // workspace: row max (fp32) in the first B*H*N floats; the fp64 denominators need 8-byte slots,

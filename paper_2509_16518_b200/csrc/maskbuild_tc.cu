@@ -1,0 +1,371 @@
+// K1a cached-threshold builder on the tensor cores (M = 128, D in {64, 128}).
+//
+// Reference: oracle.py:45-52 (attention_map: s = (q k^T) * scale, a = exp(s - max_row) /
+// sum_row in fp64, as fp32) + masks.py:66-72 (_group_max over a group's rows, after the
+// bf16 rounding of analysis_scores, core.py:196-200), used by build_mask_cached
+// (masks.py:94-105); paths relative to /root/reference/pkg/src/sliceattn/.
+//
+// The CUDA-core version (maskbuild.cu) streams Q K^T three times through FP32 FMA chains
+// (~0.4 s at Wan 480p).  Here every score tile is a tcgen05 SS-MMA (bf16 x bf16 products
+// are exact in fp32; only the accumulation order differs from NumPy's BLAS) and the
+// per-element work stays in fp32/fp64 on the CUDA cores:
+//
+//   pass 0 (rows):  S = Q_t K_c^T, thread = query row.  Running row max m and the
+//                   denominator sum_j exp(s_ij - m) (per-chunk fp32 partial sums of MUFU
+//                   ex2 terms, accumulated and rescaled in fp64); writes m_i and 1/den_i.
+//   pass 1 (group): S^T = K_c Q_g^T, thread = key j, columns = the group's 128 queries.
+//                   The transposed tile turns the column max over a group into a per-thread
+//                   max: select i* = argmax_i s_ij - (m_i + ln den_i) (one FFMA and a compare
+//                   per element, no exp), then gmax_gj = expf(s_i*j - m_i*) / den_i* evaluated
+//                   as the reference does, bf16-rounded.
+//
+// Warps (18, one CTA per SM, persistent over (b, h, tile) units): 0-15 epilogue (four per TMEM
+// lane quadrant, 32 columns each), 16 MMA issuer, 17 TMA producer (Q tile + 4-slot K ring).
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include "attn_common.cuh"
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace fga {
+namespace {
+
+constexpr int CB_EW = 4;              // epilogue warps per TMEM lane quadrant
+constexpr int CB_EPI = 4 * CB_EW;      // epilogue warps 0..15
+constexpr int CB_WARPS = CB_EPI + 2;   // + MMA issuer + TMA producer
+constexpr int CB_NS = 4;  // K ring slots
+constexpr int CB_BARS = 2 + 2 * CB_NS + 4;
+
+template <int D>
+struct CbSmem {
+  static constexpr int KV = (D / 64) * HALF;  // one 128-row tile
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = KV;
+  static constexpr int OFF_BAR = OFF_K + CB_NS * KV;
+  static constexpr int OFF_TAB = OFF_BAR + 256;       // pass 1: (m_i, 1/den_i, m_i + ln den_i) per query
+  static constexpr int OFF_XCH = OFF_TAB + 128 * 16;  // pass 0: (m, den) per slice; pass 1: candidates x 2
+  static constexpr int BYTES = OFF_XCH + 2 * 3 * CB_EW * 128 * 4;
+  static_assert(CB_EW * 128 * 12 <= 2 * 3 * CB_EW * 128 * 4, "exchange area");
+  static_assert(CB_BARS * 8 + 8 <= 256, "barrier area");
+};
+
+struct CbBars {
+  uint64_t *q_full, *q_empty, *k_full, *k_empty, *s_full, *s_empty;
+  uint32_t* tmem_slot;
+};
+
+template <int D>
+__device__ __forceinline__ CbBars cb_bars(uint8_t* smem) {
+  uint64_t* b = reinterpret_cast<uint64_t*>(smem + CbSmem<D>::OFF_BAR);
+  CbBars r;
+  r.q_full = b;
+  r.q_empty = b + 1;
+  r.k_full = b + 2;
+  r.k_empty = r.k_full + CB_NS;
+  r.s_full = r.k_empty + CB_NS;
+  r.s_empty = r.s_full + 2;
+  r.tmem_slot = reinterpret_cast<uint32_t*>(r.s_empty + 2);
+  return r;
+}
+
+struct CbParams {
+  int64_t bh;   // B * H
+  int n;        // sequence length
+  int tiles;    // ceil(n / 128): query tiles = groups (M = 128)
+  float scale;
+  int round;
+  float* row_max;  // [B*H*N]
+  float* row_rinv; // [B*H*N]
+  float* gmax;     // [B*H*G*N]
+};
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * CB_EPI) : "memory"); }
+
+template <int D, int PASS>
+__global__ void __launch_bounds__(32 * CB_WARPS, 1)
+    cached_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const CbParams p) {
+  using L = CbSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_cb[];
+  uint8_t* smem = smem_cb;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+  const CbBars bar = cb_bars<D>(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t n_units = p.bh * p.tiles;
+  const int nch = p.tiles;  // key chunks per unit
+  if (tid == 0) {
+    prefetch_tmap(&tmQ);
+    prefetch_tmap(&tmK);
+    mbar_init(bar.q_full, 1);
+    mbar_init(bar.q_empty, 1);
+    for (int i = 0; i < CB_NS; ++i) {
+      mbar_init(&bar.k_full[i], 1);
+      mbar_init(&bar.k_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar.s_full[i], 1);
+      mbar_init(&bar.s_empty[i], CB_EPI);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    tmem_alloc(bar.tmem_slot, 256);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *bar.tmem_slot;
+
+  if (warp == CB_EPI + 1) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      const uint64_t pol_q = policy_evict_first(), pol_k = policy_evict_last();
+      uint32_t kc = 0;
+      int it = 0;
+      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+        const int64_t bh = u / p.tiles;
+        const int t = static_cast<int>(u % p.tiles);
+        const int row0 = static_cast<int>(bh * p.n);
+        mbar_wait(bar.q_empty, (it & 1) ^ 1);
+        mbar_expect_tx(bar.q_full, BM * D * 2);
+#pragma unroll
+        for (int h = 0; h < D / 64; ++h) tma_load_2d(smem + L::OFF_Q + h * HALF, &tmQ, bar.q_full, h * 64, row0 + t * BM, pol_q);
+        for (int c = 0; c < nch; ++c, ++kc) {
+          const uint32_t slot = kc % CB_NS, use = kc / CB_NS;
+          mbar_wait(&bar.k_empty[slot], (use & 1) ^ 1);
+          mbar_expect_tx(&bar.k_full[slot], BN * D * 2);
+#pragma unroll
+          for (int h = 0; h < D / 64; ++h)
+            tma_load_2d(smem + L::OFF_K + slot * L::KV + h * HALF, &tmK, &bar.k_full[slot], h * 64, row0 + c * BN, pol_k);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == CB_EPI) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t IDESC = idesc_bf16(BM, BN, false, false);  // both operands K-major in SMEM
+    const uint64_t dq0 = sdesc_sw128(smem_u32(smem + L::OFF_Q), 16, 1024);
+    const uint64_t dk0 = sdesc_sw128(smem_u32(smem + L::OFF_K), 16, 1024);
+    uint32_t kc = 0, sc = 0;
+    int it = 0;
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+      mbar_wait(bar.q_full, it & 1);
+      for (int c = 0; c < nch; ++c, ++kc, ++sc) {
+        const uint32_t slot = kc % CB_NS, use = kc / CB_NS, b = sc & 1;
+        mbar_wait(&bar.k_full[slot], use & 1);
+        mbar_wait(&bar.s_empty[b], ((sc >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
+            if (PASS == 0) umma_ss(tmem + b * 128, dq0 + off, dk + off, IDESC, kk > 0 ? 1u : 0u);  // S = Q K^T
+            else umma_ss(tmem + b * 128, dk + off, dq0 + off, IDESC, kk > 0 ? 1u : 0u);           // S^T = K Q^T
+          }
+          umma_commit(&bar.s_full[b]);
+          umma_commit(&bar.k_empty[slot]);
+          if (c == nch - 1) umma_commit(bar.q_empty);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp < CB_EPI) {
+    // ---------------------------------------------------------------- epilogue
+    // warp (w, q): TMEM lane quadrant q, columns [32w, 32w + 32) of the 128-column tile
+    const int q = warp & 3, w = warp >> 2;
+    const int row = q * 32 + lane;  // TMEM lane: query row (pass 0) or key row (pass 1)
+    const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16) + w * 32;
+    const float4* tab = reinterpret_cast<const float4*>(smem + L::OFF_TAB);
+    uint32_t sc = 0;
+    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int64_t bh = u / p.tiles;
+      const int t = static_cast<int>(u % p.tiles);
+      const int64_t row0 = bh * p.n;
+      const int q0 = t * BM;
+      if (PASS == 1) {
+        // the group's (m_i, 1/den_i, m_i + ln den_i); rows past the sequence end are never selected
+        if (tid < 128) {
+          const int i = q0 + tid;
+          float4 e = make_float4(0.f, 0.f, INFINITY, 0.f);
+          if (i < p.n) {
+            const float mi = p.row_max[row0 + i], ri = p.row_rinv[row0 + i];
+            e = make_float4(mi, ri, mi - logf(ri), 0.f);
+          }
+          reinterpret_cast<float4*>(smem + L::OFF_TAB)[tid] = e;
+        }
+        epi_bar();
+      }
+      float m = -INFINITY;
+      double den = 0.0;
+      for (int c = 0; c < nch; ++c, ++sc) {
+        const uint32_t b = sc & 1;
+        mbar_wait(&bar.s_full[b], (sc >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[32];
+        tmem_ld32(tl + b * 128, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar.s_empty[b]);
+        if (PASS == 0) {
+          // columns: keys j = c*128 + 32w + k; s = fl(acc * scale) as attention_map's _scores
+          const int jbase = c * BN + w * 32;
+          float s[32];
+          float cmax = -INFINITY;
+          if (jbase + 32 <= p.n) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              s[k] = __fmul_rn(__uint_as_float(v[k]), p.scale);
+              cmax = fmaxf(cmax, s[k]);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              s[k] = jbase + k < p.n ? __fmul_rn(__uint_as_float(v[k]), p.scale) : -INFINITY;
+              cmax = fmaxf(cmax, s[k]);
+            }
+          }
+          if (cmax > m) {
+            den = m == -INFINITY ? 0.0 : den * exp(static_cast<double>(m) - static_cast<double>(cmax));
+            m = cmax;
+          }
+          if (m != -INFINITY) {  // (columns entirely past the sequence end add nothing)
+            // terms exp(s - m) by MUFU ex2 on (s - m) * log2e; their rounding errors average out
+            // over the row's N terms, each chunk's 32 summed in fp32, the row in fp64
+            const float ml = m * 1.4426950408889634f;
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              const float2 x = __ffma2_rn(make_float2(s[k], s[k + 1]), make_float2(1.4426950408889634f, 1.4426950408889634f),
+                                          make_float2(-ml, -ml));
+              acc = __fadd2_rn(acc, make_float2(ex2(x.x), ex2(x.y)));
+            }
+            den += static_cast<double>(acc.x) + static_cast<double>(acc.y);
+          }
+        } else {
+          // columns: the group's queries i = 32w + k; row: key j = c*128 + row.  Select the query
+          // maximising s_ij - (m_i + ln den_i), then evaluate a_ij = expf(s_ij - m_i) / den_i exactly
+          // as the reference does for that one query.
+          float by = -INFINITY, bacc = 0.f;
+          int bi = 0;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float y = fmaf(__uint_as_float(v[k]), p.scale, -tab[w * 32 + k].z);
+            if (y > by) {
+              by = y;
+              bacc = __uint_as_float(v[k]);
+              bi = w * 32 + k;
+            }
+          }
+          float* xy = reinterpret_cast<float*>(smem + L::OFF_XCH) + (sc & 1) * (3 * CB_EW * 128);
+          if (w > 0) {
+            xy[(w * 3 + 0) * 128 + row] = by;
+            xy[(w * 3 + 1) * 128 + row] = bacc;
+            xy[(w * 3 + 2) * 128 + row] = __int_as_float(bi);
+          }
+          epi_bar();  // double-buffered by chunk parity: one barrier per chunk
+          if (w == 0) {
+#pragma unroll
+            for (int o = 1; o < CB_EW; ++o) {
+              const float yo = xy[(o * 3 + 0) * 128 + row];
+              if (yo > by) {
+                by = yo;
+                bacc = xy[(o * 3 + 1) * 128 + row];
+                bi = __float_as_int(xy[(o * 3 + 2) * 128 + row]);
+              }
+            }
+            const float4 e = tab[bi];
+            float g = __fmul_rn(expf(__fsub_rn(__fmul_rn(bacc, p.scale), e.x)), e.y);
+            if (p.round) g = __bfloat162float(__float2bfloat16_rn(g));
+            const int j = c * BN + row;
+            if (j < p.n) p.gmax[(bh * p.tiles + t) * static_cast<int64_t>(p.n) + j] = g;
+          }
+        }
+      }
+      if (PASS == 0) {
+        // merge the column slices of each row: den relative to the common max
+        float* xf = reinterpret_cast<float*>(smem + L::OFF_XCH);
+        double* xd = reinterpret_cast<double*>(smem + L::OFF_XCH + CB_EW * 128 * 4);
+        if (w > 0) {
+          xf[w * 128 + row] = m;
+          xd[w * 128 + row] = den;
+        }
+        epi_bar();
+        if (w == 0) {
+          float mx = m;
+#pragma unroll
+          for (int o = 1; o < CB_EW; ++o) mx = fmaxf(mx, xf[o * 128 + row]);
+          double tot = m == -INFINITY ? 0.0 : den * exp(static_cast<double>(m) - static_cast<double>(mx));
+#pragma unroll
+          for (int o = 1; o < CB_EW; ++o) {
+            const float mo = xf[o * 128 + row];
+            if (mo != -INFINITY) tot += xd[o * 128 + row] * exp(static_cast<double>(mo) - static_cast<double>(mx));
+          }
+          const int i = q0 + row;
+          if (i < p.n) {
+            p.row_max[row0 + i] = mx;
+            p.row_rinv[row0 + i] = static_cast<float>(1.0 / tot);
+          }
+        }
+      }
+      epi_bar();  // exchange / table space free for the next unit
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+template <int D, int PASS>
+int launch_pass(const CUtensorMap* maps, const CbParams& p, cudaStream_t st) {
+  auto kern = cached_tc_kernel<D, PASS>;
+  const int smem = CbSmem<D>::BYTES;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return check_launch("cudaFuncSetAttribute(cached_tc)");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t units = p.bh * p.tiles;
+  kern<<<static_cast<unsigned>(units < sms ? units : sms), 32 * CB_WARPS, smem, st>>>(maps[0], maps[1], p);
+  return check_launch("cached_tc_kernel");
+}
+
+}  // namespace
+
+// Tensor-core cached builder; returns FGA_EUNSUPPORTED (caller uses the CUDA-core kernel)
+// unless M == 128 and D is 64 or 128.
+int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s, int round, float* gmax,
+                               float* row_max, cudaStream_t st) {
+  const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
+  if (M != 128 || (D != 64 && D != 128)) return FGA_EUNSUPPORTED;
+  const int64_t rows = B * H * N;
+  if (rows >= (int64_t(1) << 31)) return FGA_EUNSUPPORTED;
+  CUtensorMap maps[2];
+  int rc;
+  if ((rc = make_tmap_bf16_2d(&maps[0], q, rows, D, 64, BM)) != FGA_OK) return rc;
+  if ((rc = make_tmap_bf16_2d(&maps[1], k, rows, D, 64, BN)) != FGA_OK) return rc;
+  float* rinv = nullptr;
+  if (cudaMallocAsync(&rinv, sizeof(float) * rows, st) != cudaSuccess) return check_launch("cudaMallocAsync");
+  CbParams p{};
+  p.bh = B * H;
+  p.n = static_cast<int>(N);
+  p.tiles = static_cast<int>((N + BM - 1) / BM);
+  p.scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
+  p.round = round;
+  p.row_max = row_max;
+  p.row_rinv = rinv;
+  p.gmax = gmax;
+  rc = D == 64 ? launch_pass<64, 0>(maps, p, st) : launch_pass<128, 0>(maps, p, st);
+  if (rc == FGA_OK) rc = D == 64 ? launch_pass<64, 1>(maps, p, st) : launch_pass<128, 1>(maps, p, st);
+  cudaFreeAsync(rinv, st);
+  return rc;
+}
+
+}  // namespace fga

@@ -323,6 +323,35 @@ def test_cached_group_max(golden):
     assert (flips <= mism).all()
 
 
+@pytest.mark.parametrize("n,d,h", [(1000, 128, 2), (640, 64, 3), (200, 128, 1)])
+def test_cached_group_max_tensor_cores_vs_oracle(n, d, h, monkeypatch):
+    # ragged N (last group / key chunk partial), both head dims; the tensor-core passes
+    # (maskbuild_tc.cu) and the CUDA-core passes (FGA_CACHED_CC=1) against the NumPy map
+    m, b = 128, 1
+    q = oracle.bf16_round(oracle.gaussian((b, h, n, d), 11))
+    k = oracle.bf16_round(oracle.gaussian((b, h, n, d), 12))
+    amap = oracle.attention_map(q, k, None, "bf16")
+    tau = 2.0 / n
+    keep_ref, ref = oracle.cached_keep(amap, m, tau, "bf16")
+    gc = oracle.num_groups(n, m)
+    qd, kd = to_bf16_dev(q), to_bf16_dev(k)
+    for cc in ("0", "1"):
+        monkeypatch.setenv("FGA_CACHED_CC", cc)
+        gmax = torch.full((b, h, gc, n), -1.0, device="cuda", dtype=torch.float32)
+        ws = torch.empty(2 * b * h * n, device="cuda", dtype=torch.float32)
+        _lib.call("fga_cached_group_max", ptr(qd), ptr(kd), _lib.shape(b, h, n, d, m), 1, ptr(gmax), ptr(ws), stream())
+        torch.cuda.synchronize()
+        got = gmax.cpu().numpy()
+        mism = got != ref
+        assert mism.mean() < 1e-3, (cc, mism.mean())
+        # where they differ, by one bf16 step at most
+        if mism.any():
+            rel = np.abs(got[mism] - ref[mism]) / np.maximum(np.abs(ref[mism]), 1e-30)
+            assert rel.max() <= 2 ** -7, (cc, rel.max())
+        flips = (got >= tau) != keep_ref
+        assert (flips <= mism).all(), cc
+
+
 def test_random_keep_exact_counts():
     rows, n, count = 64, 32760, 14742
     keep = torch.empty((rows, n), dtype=torch.uint8, device="cuda")
