@@ -75,33 +75,64 @@ __device__ __forceinline__ void dot_tile(LA la, LB lb, int D, float (&acc)[4][4]
   }
 }
 
-// scores[bh, g, j] for a 64(g) x 64(j) tile.  grid: (key tiles, group tiles, B*H)
-__global__ void __launch_bounds__(256) pooled_scores_kernel(const float* __restrict__ qbar,
-                                                            const __nv_bfloat16* __restrict__ k,
-                                                            float* __restrict__ scores, int N, int D, int G,
-                                                            float scale, int round) {
+// scores[bh, g, j] for a 128(g) x 128(j) tile, 256 threads x (8 x 8): each thread reads
+// 4 float4 of the transposed SMEM tiles per d and issues 64 FMAs (FMA-bound, not LDS-bound);
+// the per-score FMA chain still runs over d in ascending order.  grid: (key tiles, group tiles, B*H)
+constexpr int PT = 128, PDK = 32, PPAD = 4;
+__global__ void __launch_bounds__(256) pooled_scores128_kernel(const float* __restrict__ qbar,
+                                                               const __nv_bfloat16* __restrict__ k,
+                                                               float* __restrict__ scores, int N, int D, int G,
+                                                               float scale, int round) {
+  __shared__ __align__(16) float As[PDK][PT + PPAD];  // [d][g]
+  __shared__ __align__(16) float Bs[PDK][PT + PPAD];  // [d][j]
   const int64_t bh = blockIdx.z;
-  const int g0 = blockIdx.y * TILE, j0 = blockIdx.x * TILE;
-  float acc[4][4];
-  dot_tile(
-      [&](int r, int d) { const int g = g0 + r; return g < G ? qbar[(bh * G + g) * D + d] : 0.f; },
-      [&](int r, int d) { const int j = j0 + r; return j < N ? ld_bf16(k + (bh * N + j) * D + d) : 0.f; }, D, acc);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const float inv_d = static_cast<float>(D);
+  const int g0 = blockIdx.y * PT, j0 = blockIdx.x * PT;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  float acc[8][8];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int g = g0 + ty + 16 * r;
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[r][c] = 0.f;
+  for (int d0 = 0; d0 < D; d0 += PDK) {
+    // stage: thread t loads row (t / 2) ... 16 consecutive d of 128 rows -> transposed stores
+    for (int e = tid; e < PT * PDK; e += 256) {
+      const int rr = e / PDK, dd = e % PDK;
+      const int g = g0 + rr, j = j0 + rr;
+      As[dd][rr] = g < G ? qbar[(bh * G + g) * D + d0 + dd] : 0.f;
+      Bs[dd][rr] = j < N ? ld_bf16(k + (bh * N + j) * D + d0 + dd) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int dd = 0; dd < PDK; ++dd) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[dd][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[dd][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[dd][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[dd][64 + tx * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[r][c] = __fmaf_rn(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+  const float dd = static_cast<float>(D);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int g = g0 + (r < 4 ? ty * 4 + r : 64 + ty * 4 + r - 4);
     if (g >= G) continue;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = j0 + tx + 16 * c;
+    for (int c = 0; c < 8; ++c) {
+      const int j = j0 + (c < 4 ? tx * 4 + c : 64 + tx * 4 + c - 4);
       if (j >= N) continue;
-      float s = __fdiv_rn(expf(__fmul_rn(acc[r][c], scale)), inv_d);
+      float s = __fdiv_rn(expf(__fmul_rn(acc[r][c], scale)), dd);
       if (round) s = bf16_rne(s);
       scores[(bh * G + g) * N + j] = s;
     }
   }
 }
+
 
 // ------------------------------------------------------------ group max of an explicit map
 __global__ void group_max_map_kernel(const float* __restrict__ map, int64_t n, int64_t m, int64_t g_count,
@@ -333,12 +364,12 @@ int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int r
       static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N), static_cast<int>(D), static_cast<int>(M),
       static_cast<int>(G));
   const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
-  dim3 grid(static_cast<unsigned>((N + TILE - 1) / TILE), static_cast<unsigned>((G + TILE - 1) / TILE),
+  dim3 grid(static_cast<unsigned>((N + PT - 1) / PT), static_cast<unsigned>((G + PT - 1) / PT),
             static_cast<unsigned>(B * H));
-  pooled_scores_kernel<<<grid, 256, 0, st>>>(qbar, static_cast<const __nv_bfloat16*>(k), scores,
-                                             static_cast<int>(N), static_cast<int>(D), static_cast<int>(G), scale,
-                                             round);
-  int rc = check_launch("pooled_scores_kernel");
+  pooled_scores128_kernel<<<grid, 256, 0, st>>>(qbar, static_cast<const __nv_bfloat16*>(k), scores,
+                                                static_cast<int>(N), static_cast<int>(D), static_cast<int>(G), scale,
+                                                round);
+  int rc = check_launch("pooled_scores128_kernel");
   cudaFreeAsync(qbar, st);
   return rc;
 }
