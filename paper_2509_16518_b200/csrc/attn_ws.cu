@@ -82,6 +82,9 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 #ifndef FGA_NOGATHER
 #define FGA_NOGATHER 0  // timing experiments only
 #endif
+#ifndef FGA_NOMMA
+#define FGA_NOMMA 0  // timing experiments only
+#endif
 #ifndef FGA_NOEXP
 #define FGA_NOEXP 0  // timing experiments only
 #endif
@@ -386,7 +389,7 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
             const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
-            umma_ts(tS, tQ + kk * 8, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
+            if (!FGA_NOMMA) umma_ts(tS, tQ + kk * 8, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
           }
           umma_commit(&bar.s_full[r]);
           umma_commit(&bar.k_empty[slot]);
@@ -411,7 +414,8 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
         const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) umma_ts(tO, tS + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, 1u);
+          for (int kk = 0; kk < BN / 16; ++kk)
+            if (!FGA_NOMMA) umma_ts(tO, tS + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, 1u);
           umma_commit(&bar.v_empty[slot]);
           umma_commit(&bar.pv_done[r]);
         }
