@@ -124,9 +124,19 @@ def test_compact_unaligned_rows_without_scores():
 ATTN_CASES = [c for c in GOLDEN_CASES if c != "avgq_topk_ties"]
 
 
+@pytest.fixture(params=["ws", "pp"])
+def attn_kernel(request, monkeypatch):
+    """The production kernel (attn_ws.cu) and the ping-pong variant (attn_pp.cu, FGA_ATTN_KERNEL=pp)."""
+    if request.param == "pp":
+        monkeypatch.setenv("FGA_ATTN_KERNEL", "pp")
+    else:
+        monkeypatch.delenv("FGA_ATTN_KERNEL", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("name", ATTN_CASES)
 @pytest.mark.parametrize("out_f32", [True, False])
-def test_sparse_attention_matches_reference_golden(golden, name, out_f32):
+def test_sparse_attention_matches_reference_golden(golden, name, out_f32, attn_kernel):
     g = golden(name)
     b, h, n, d = g.shape
     m = g.group_size
@@ -170,7 +180,7 @@ def test_single_key_groups_copy_value_row():
 
 
 @pytest.mark.parametrize("d", [64, 128])
-def test_unsorted_duplicate_free_lists_and_stride(d):
+def test_unsorted_duplicate_free_lists_and_stride(d, attn_kernel):
     # kernel consumes lists in the given order; result is order-independent
     b, h, n, m = 1, 1, 700, 128
     rng = np.random.default_rng(d)
@@ -193,7 +203,7 @@ def test_unsorted_duplicate_free_lists_and_stride(d):
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("order", ["ascending", "descending"])
 @pytest.mark.parametrize("gain", [4.0, 16.0])
-def test_online_rescale_large_dynamic_range(d, order, gain):
+def test_online_rescale_large_dynamic_range(d, order, gain, attn_kernel):
     # Scores grow along the key list by ~50 (gain 4) or ~300 (gain 16) log2 units, so the
     # running max moves many times (the kernel's lazy-rescale slow path) -- or, descending,
     # never after the first chunk.
@@ -226,7 +236,7 @@ def test_online_rescale_large_dynamic_range(d, order, gain):
 
 
 @pytest.mark.parametrize("m", [16, 64, 200, 256])
-def test_group_sizes(m):
+def test_group_sizes(m, attn_kernel):
     b, h, n, d = 1, 2, 600, 64
     rng = np.random.default_rng(m)
     q, k, v = (oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32)) for _ in range(3))
