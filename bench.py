@@ -464,7 +464,7 @@ def extras(args, torch, np, fga, _lib, cfg, q, k, v, keep, mask, out, flops, flu
     line["e2e"] = {"value": flops / (e_ms * 1e-3) / 1e12 * world, "unit": "TFLOP/s", "ms_per_step": e_ms,
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": out.numel() * 2,
                    "path": "sparse_attention_host: pinned host Q/K/V + bit-packed slice mask -> H2D | "
-                           "fga_compact_bits + fga_sparse_attn_fwd | D2H, overlapped over 6 head slabs",
+                           "fga_compact_bits + fga_sparse_attn_fwd | D2H, overlapped over 5 head slabs (the last one a single head)",
                    "max_abs_diff_vs_device_path": e2e_err}
 
     # ---- CPU baseline (oracle port, rank 0, N=1 only) + parity of the same groups

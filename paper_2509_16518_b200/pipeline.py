@@ -36,18 +36,26 @@ def pack_keep_bits(keep):
 class HostPipeline:
     """Device buffers + streams for one problem shape (reused across calls)."""
 
-    def __init__(self, cfg: AttnConfig, slabs: int = 4, device=None):
+    def __init__(self, cfg: AttnConfig, slabs: int = 4, device=None, tail: bool = True):
         t = torch()
         self.dev = require_device(device)
         self.cfg = cfg
         bh = cfg.batch * cfg.heads
         slabs = max(1, min(slabs, bh))
-        base, extra = divmod(bh, slabs)
+        # The step costs about sum(H2D) + compute + D2H of the LAST slab (everything else hides
+        # under the next slab's upload), so with a short tail the last slab is a single head and
+        # the other heads are split evenly over the remaining slabs.
+        sizes = []
+        if tail and slabs > 1 and bh > slabs:
+            base, extra = divmod(bh - 1, slabs - 1)
+            sizes = [base + (1 if s < extra else 0) for s in range(slabs - 1)] + [1]
+        else:
+            base, extra = divmod(bh, slabs)
+            sizes = [base + (1 if s < extra else 0) for s in range(slabs)]
         self.ranges, h0 = [], 0
-        for s in range(slabs):
-            h1 = h0 + base + (1 if s < extra else 0)
-            self.ranges.append((h0, h1))
-            h0 = h1
+        for sz in sizes:
+            self.ranges.append((h0, h0 + sz))
+            h0 += sz
         n, d, g = cfg.seq_len, cfg.head_dim, cfg.num_groups
         self.words = (n + 31) // 32
         kw = dict(device=f"cuda:{self.dev}")
@@ -100,7 +108,7 @@ class HostPipeline:
 _pipes: dict = {}
 
 
-def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: int = 6):
+def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: int = 5, tail: bool = True):
     """FG-Attn from pinned host buffers (see module doc).  Returns the pinned host output;
     synchronise the current stream before reading it."""
     t = torch()
@@ -112,9 +120,9 @@ def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: 
     expect = (cfg.batch, cfg.heads, cfg.num_groups, (cfg.seq_len + 31) // 32)
     if tuple(keep_bits.shape) != expect:
         raise ShapeError(f"keep_bits must be {expect}, got {tuple(keep_bits.shape)}")
-    key = (cfg, slabs, require_device())
+    key = (cfg, slabs, tail, require_device())
     if key not in _pipes:
-        _pipes[key] = HostPipeline(cfg, slabs)
+        _pipes[key] = HostPipeline(cfg, slabs, tail=tail)
     if out is None:
         out = t.empty(cfg.dims, dtype=t.bfloat16, pin_memory=True)
     return _pipes[key](q, k, v, keep_bits, out)

@@ -16,17 +16,18 @@ bits = fga.pack_keep_bits(keep)
 hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
 hb = bits.cpu().pin_memory()
 ho = torch.empty(cfg.dims, dtype=torch.bfloat16).pin_memory()
-for slabs in [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["4", "6", "12"])]:
+for spec in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["4", "6", "12"]):
+    slabs, tail = int(spec.rstrip("u")), not spec.endswith("u")  # "6u": uniform slabs
     for _ in range(3):
-        fga.sparse_attention_host(hq, hk, hv, hb, cfg, out=ho, slabs=slabs)
+        fga.sparse_attention_host(hq, hk, hv, hb, cfg, out=ho, slabs=slabs, tail=tail)
     torch.cuda.synchronize()
     ts = []
     for _ in range(10):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fga.sparse_attention_host(hq, hk, hv, hb, cfg, out=ho, slabs=slabs)
+        fga.sparse_attention_host(hq, hk, hv, hb, cfg, out=ho, slabs=slabs, tail=tail)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     ts.sort()
-    print(f"slabs={slabs}: e2e {ts[len(ts)//2]:.3f} ms (min {ts[0]:.3f})")
+    print(f"slabs={spec}: e2e {ts[len(ts)//2]:.3f} ms (min {ts[0]:.3f})")
