@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--density", type=float, default=0.45)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--shard", default="batch", choices=["batch", "tiles"],
+                    help="batch: every rank runs its own batch element (weak scaling, default); "
+                         "tiles: one layer split over the ranks in contiguous work-balanced (head, group) "
+                         "tile ranges (strong scaling, BASELINE configs c4/c5 head-sharded)")
     ap.add_argument("--no-extras", action="store_true", help="skip dense/e2e/cpu legs (for ncu)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline work budget")
     ap.add_argument("--cpu-worker", default=None, help=argparse.SUPPRESS)
@@ -331,8 +335,19 @@ def ours(args):
     flops = rep.flops_matmul           # 4*D*pairs: the roofline numerator (softmax excluded)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step():
-        return fga.sparse_attention(q, k, v, mask, cfg)
+    strong = args.shard == "tiles"
+    if strong:
+        from paper_2509_16518_b200 import shard
+
+        ranges = shard.partition_tiles(shard.tile_work(cfg, mask.counts.cpu().numpy()), world)
+        my_range = ranges[rank]
+        out_buf = torch.zeros(cfg.dims, dtype=torch.bfloat16, device=dev)
+
+        def step():
+            return shard.sparse_attention_shard(q, k, v, mask, cfg, my_range, out_buf)
+    else:
+        def step():
+            return fga.sparse_attention(q, k, v, mask, cfg)
 
     for _ in range(args.warmup):
         step()
@@ -356,16 +371,19 @@ def ours(args):
     torch.cuda.synchronize()
 
     peak, peak_sus, hbm_peak, peak_src = measured_peaks()
-    achieved = flops / (kernel_ms * 1e-3) / 1e12
+    achieved = flops / (kernel_ms * 1e-3) / 1e12  # strong: the whole layer's FLOPs in the slowest rank's time
     gathered = int(rep.density * cfg.batch * heads * cfg.num_groups * n) * 4 * d  # K + V rows, bf16
-    value = achieved * world
+    value = achieved if strong else achieved * world
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": kernel_ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": kernel_ms, "higher_is_better": True, "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (N(0,1) bf16 Q/K/V, uniform random slice mask)",
-        "config": {"workload": desc, "config": args.config, "batch_per_gpu": 1, "global_batch": world,
+        "config": {"workload": desc, "config": args.config, "batch_per_gpu": 1 if not strong else None,
+                   "global_batch": 1 if strong else world,
                    "heads": heads, "seq_len": n, "head_dim": d, "group_size": m, "density": args.density,
-                   "keys_per_group": count, "parallelism": f"dp{world} (batch-sharded, weak)",
+                   "keys_per_group": count,
+                   "parallelism": (f"tiles{world} (one layer, work-balanced (head, group) tile ranges, strong)" if strong
+                                   else f"dp{world} (batch-sharded, weak)"),
                    "l2": "flushed between steps (512 MiB write, untimed)"},
         "latency_ms": kernel_ms,
         "gpu_launches": args.steps,
@@ -384,8 +402,17 @@ def ours(args):
         "wall_s_timed_region": wall,
     }
 
-    # ---- validation all-gather (NCCL, outside the timed region): bitwise equal across ranks
-    if dist:
+    # ---- validation (NCCL, outside the timed region)
+    if strong:
+        # the ranks' tile ranges, summed over ranks (zeros elsewhere), must equal the one-GPU layer bitwise
+        full = fga.sparse_attention(q, k, v, mask, cfg)
+        red = out_buf.clone()
+        if dist:
+            dist.all_reduce(red)
+        line["reassembled_bitwise_equal"] = bool(torch.equal(red, full))
+        line["tile_ranges"] = ranges
+        out = full
+    elif dist:
         from paper_2509_16518_b200.shard import gather_outputs
 
         sample = out[0, 0, :256].contiguous()

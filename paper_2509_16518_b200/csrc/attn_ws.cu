@@ -82,6 +82,9 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 #ifndef FGA_NOGATHER
 #define FGA_NOGATHER 0  // timing experiments only
 #endif
+#ifndef FGA_PV_ORDER
+#define FGA_PV_ORDER 1  // PVs issued in chunk order across the two issuers (bitwise-reproducible O)
+#endif
 #ifndef FGA_NOMMA
 #define FGA_NOMMA 0  // timing experiments only
 #endif
@@ -107,7 +110,7 @@ struct WsSmem {
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + NSK * KV;
   static constexpr int OFF_BAR = OFF_V + NSV * KV;
-  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3;
+  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3 + 1;
   static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row
   static constexpr int BYTES = OFF_XCH + 2 * 128 * 4;
   // The two issuers free a ring's slots in chunk order only up to swaps of neighbouring
@@ -127,6 +130,7 @@ struct Bars {
   uint64_t* s_full;    // [2]
   uint64_t* p_full;    // [2] count 8 (every softmax warp)
   uint64_t* pv_done;   // [2] completion of PV into S buffer b's P
+  uint64_t* pv_issued; // count 1: PV_c has been issued (PVs enter the tensor pipe in chunk order)
   uint64_t* q_full;    // count 8 (every softmax warp writes a part of Q)
   uint64_t* o_full;
   uint64_t* o_empty;   // count 8
@@ -148,7 +152,8 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   r.q_full = r.pv_done + 2;
   r.o_full = r.q_full + 1;
   r.o_empty = r.o_full + 1;
-  r.tmem_slot = reinterpret_cast<uint32_t*>(r.o_empty + 1);
+  r.pv_issued = r.o_empty + 1;
+  r.tmem_slot = reinterpret_cast<uint32_t*>(r.pv_issued + 1);
   return r;
 }
 
@@ -412,12 +417,16 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
         fence_proxy_async_smem();
         tc_fence_after();
         const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
+        // Deterministic accumulation: PV_c enters the tensor pipe only after PV_{c-1} (the other
+        // issuer's) has been issued, so O sums the chunks in list order on every run.
+        if (FGA_PV_ORDER && c > 0) mbar_wait(bar.pv_issued, (c - 1) & 1);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
             if (!FGA_NOMMA) umma_ts(tO, tS + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, 1u);
           umma_commit(&bar.v_empty[slot]);
           umma_commit(&bar.pv_done[r]);
+          if (FGA_PV_ORDER) mbar_arrive(bar.pv_issued);
         }
         __syncwarp();
         if (r == 0) FGA_TS(p, it, j, 12);
@@ -744,6 +753,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     mbar_init(bar.q_full, NSOFT);
     mbar_init(bar.o_full, 2);
     mbar_init(bar.o_empty, NSOFT);
+    mbar_init(bar.pv_issued, 1);
     fence_barrier_init();
   }
   if (warp == 0) {

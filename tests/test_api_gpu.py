@@ -193,3 +193,15 @@ def test_host_pipeline_equals_device_path():
         out = fga.sparse_attention_host(hq, hk, hv, hb, cfg, slabs=slabs)
         torch.cuda.synchronize()
         assert torch.equal(out, ref.cpu()), slabs
+
+
+def test_sparse_attention_is_bitwise_reproducible():
+    # the two MMA issuers issue their PVs in chunk order (FGA_PV_ORDER), so O accumulates the
+    # chunks in list order on every run (without it ~1e-6 of the outputs flip between runs)
+    cfg = fga.AttnConfig(1, 4, 32760, 128, precision="bf16")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v = (torch.randn(cfg.dims, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    m = fga.random_mask_device(cfg, 0.45, seed=2)
+    ref = fga.sparse_attention(q, k, v, m, cfg)
+    for _ in range(4):
+        assert torch.equal(fga.sparse_attention(q, k, v, m, cfg), ref)
