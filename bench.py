@@ -15,7 +15,11 @@ the timed events.  ``value`` = algorithmic TFLOP/s = 4*D*sum(rows_g*count_g)
 process per GPU (torchrun), every rank runs its own batch element of the
 layer (weak scaling, no collective on the hot path); NCCL is used only to
 take the max time over ranks and to all-gather an output sample for the
-bitwise cross-rank check.
+bitwise cross-rank check.  ``--shard tiles`` instead splits ONE layer over the
+ranks in contiguous work-balanced (head, group) tile ranges (strong scaling,
+BASELINE configs c4/c5 "head-sharded"): value = the layer's FLOPs / the
+slowest rank's time, and the ranks' outputs are NCCL-summed and checked
+bitwise against a one-GPU run of the layer.
 
 ``e2e`` is the same metric through the public API from pinned HOST buffers
 (``sparse_attention_host``): per step H2D of Q/K/V and the bit-packed slice
