@@ -21,7 +21,7 @@ from .perfmodel import CostReport, count_flops, flop_speedup, synthetic_trace, t
 from .sparse import (DeviceIndexMask, PackedTile, SparseIndexMask, compact_keep, compact_keep_bits, export_padded, full_mask,
                      gather_rows, import_padded, mask_density, mask_jaccard, masked_dense_attention, random_mask,
                      random_mask_device, sparse_attention)
-from .tiled import dense_attention, flash_attention
+from .tiled import OnlineSoftmaxState, dense_attention, finalize, flash_attention, init_state, online_softmax_update
 from . import io  # noqa: E402  (FGT1 / FGM1 formats)
 from .stream import IterStreamConfig, generate_stream, run_cached_pipeline
 

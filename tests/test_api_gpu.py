@@ -205,3 +205,24 @@ def test_sparse_attention_is_bitwise_reproducible():
     ref = fga.sparse_attention(q, k, v, m, cfg)
     for _ in range(4):
         assert torch.equal(fga.sparse_attention(q, k, v, m, cfg), ref)
+
+
+def test_online_softmax_primitives_match_one_shot_softmax():
+    # tiled.py:27-77 semantics: folding tiles == softmax over their concatenation; the -inf guard
+    rng = np.random.default_rng(4)
+    rows, d = 16, 64
+    tiles = [rng.standard_normal((rows, w)).astype(np.float32) * 3 for w in (5, 128, 1, 40)]
+    vals = [rng.standard_normal((w, d)).astype(np.float32) for w in (5, 128, 1, 40)]
+    tiles[0][3] = -np.inf  # a row with no finite score in the first tile
+    st = fga.init_state(rows, d)
+    for s, v in zip(tiles, vals):
+        st = fga.online_softmax_update(st, s, v)
+    out = fga.finalize(st).cpu().numpy()
+    s_all, v_all = np.concatenate(tiles, 1).astype(np.float64), np.concatenate(vals, 0).astype(np.float64)
+    p = np.exp(s_all - s_all.max(1, keepdims=True))
+    ref = (p / p.sum(1, keepdims=True)) @ v_all
+    assert np.abs(out - ref).max() < 1e-5
+    with pytest.raises(fga.NumericError):
+        fga.finalize(fga.init_state(2, 4))
+    with pytest.raises(fga.ShapeError):
+        fga.online_softmax_update(fga.init_state(2, 4), np.zeros((2, 3), np.float32), np.zeros((2, 4), np.float32))
