@@ -48,9 +48,23 @@ constexpr int WARP_MMA0 = 8;    // MMA issuers 8 (buffer 0) and 9 (buffer 1)
 constexpr int WARP_PROD0 = 10;
 constexpr int NPK = 3;          // producer warps of the K ring = its slots (one warp per slot)
 constexpr int NPV = 3;          // producer warps of the V ring = its slots
-constexpr int NWARPS = 16;
-constexpr int REG_SOFTMAX = 184;
-constexpr int REG_OTHER = 72;
+#ifndef FGA_EPI_WARPS
+#define FGA_EPI_WARPS 0  // 1: four dedicated epilogue warps (16-19) finish each tile off the softmax's path (measured slower: any 20-warp build is)
+#endif
+#ifndef FGA_NW20
+#define FGA_NW20 0  // timing experiment: 20 warps (register split of the epilogue build) without the role
+#endif
+constexpr bool kWide = FGA_EPI_WARPS || FGA_NW20;
+constexpr int NWARPS = kWide ? 20 : 16;
+constexpr int WARP_EPI0 = 16;
+#ifndef FGA_REG_SOFTMAX
+#define FGA_REG_SOFTMAX (kWide ? 144 : 184)
+#endif
+#ifndef FGA_REG_OTHER
+#define FGA_REG_OTHER (kWide ? 64 : 72)
+#endif
+constexpr int REG_SOFTMAX = FGA_REG_SOFTMAX;
+constexpr int REG_OTHER = FGA_REG_OTHER;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units (factor 256)
 constexpr float RESCALE_SUM = 256.0f;      // 2^RESCALE_THRESHOLD
 constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
@@ -110,9 +124,9 @@ struct WsSmem {
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + NSK * KV;
   static constexpr int OFF_BAR = OFF_V + NSV * KV;
-  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3 + 1;
-  static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row
-  static constexpr int BYTES = OFF_XCH + 2 * 128 * 4;
+  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3 + 1 + 4;
+  static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row, x2 tiles
+  static constexpr int BYTES = OFF_XCH + 2 * 2 * 128 * 4;
   // The two issuers free a ring's slots in chunk order only up to swaps of neighbouring
   // chunks (c and c+1 come from different issuers).  With one producer warp per slot a
   // producer waits only for its own slot's previous use, which it issued itself after the
@@ -131,6 +145,8 @@ struct Bars {
   uint64_t* p_full;    // [2] count 8 (every softmax warp)
   uint64_t* pv_done;   // [2] completion of PV into S buffer b's P
   uint64_t* pv_issued; // count 1: PV_c has been issued (PVs enter the tensor pipe in chunk order)
+  uint64_t* stats_full;   // [2] count 8: the softmax warps published (m, l) of tile it (buffer it % 2)
+  uint64_t* stats_empty;  // [2] count 4: the epilogue warps read them
   uint64_t* q_full;    // count 8 (every softmax warp writes a part of Q)
   uint64_t* o_full;
   uint64_t* o_empty;   // count 8
@@ -153,7 +169,9 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   r.o_full = r.q_full + 1;
   r.o_empty = r.o_full + 1;
   r.pv_issued = r.o_empty + 1;
-  r.tmem_slot = reinterpret_cast<uint32_t*>(r.pv_issued + 1);
+  r.stats_full = r.pv_issued + 1;
+  r.stats_empty = r.stats_full + 2;
+  r.tmem_slot = reinterpret_cast<uint32_t*>(r.stats_empty + 2);
   return r;
 }
 
@@ -533,14 +551,16 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
   int64_t tile = p.tile_begin + blockIdx.x;
   if (tile < p.n_tiles) {
     write_q<D>(p, qptr, decode_tile(p, tile), tmem, q, h, lane);
+    if (!FGA_EPI_WARPS) {
 #pragma unroll
-    for (int i = 0; i < NQ32; ++i) tmem_st32(tOw + i * 32, zero);  // every PV accumulates into O
+      for (int i = 0; i < NQ32; ++i) tmem_st32(tOw + i * 32, zero);  // every PV accumulates into O
+    }
     tmem_st_wait();
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
       mbar_arrive(bar.q_full);
-      mbar_arrive(bar.o_empty);
+      if (!FGA_EPI_WARPS) mbar_arrive(bar.o_empty);
     }
   }
   for (; tile < p.n_tiles; tile += gridDim.x, ++it) {
@@ -680,11 +700,27 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
     for (int r = 0; r < 2; ++r) {
       l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 1);
       l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 2);
+    }
+    if (FGA_EPI_WARPS) {
+      // hand (m, l) to the epilogue warps through buffer it % 2 and go on with the next tile
+      const int buf = it & 1;
+      if (it >= 2) mbar_wait(&bar.stats_empty[buf], ((it >> 1) - 1) & 1);
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+        if (a == 0) {
+          xch[buf * 256 + r0 + 8 * r] = m_use[r];
+          xch[buf * 256 + 128 + r0 + 8 * r] = l_run[r];
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar.stats_full[buf]);
+      continue;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
       if (a == 0) {
         xch[r0 + 8 * r] = m_use[r];
         xch[128 + r0 + 8 * r] = l_run[r];
       }
-    }
     softmax_bar();
     const int row = q * 32 + lane;
     const float mrow = xch[row], lrow = xch[128 + row];
@@ -711,6 +747,57 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
     if (h == 0 && valid && p.lse != nullptr)
       p.lse[out_row] = lrow > 0.f ? mrow * 0.69314718055994531f + logf(lrow) : -INFINITY;
     if (tid == 0) FGA_TT(p, it, 5);
+  }
+}
+
+// ------------------------------------------------------------------ epilogue warps
+// Warp 16 + q (TMEM lane quadrant q, thread = query row): per tile, wait for the softmax's
+// (m, l) and for the tile's last PV, then read O 32 columns at a time, clear it, release it to
+// the next tile's PVs (o_empty) and store O / l (tiled.py:73-77) and the LSE.  The softmax
+// warps meanwhile start on the next tile.
+template <int D, bool OUT_F32>
+__device__ __forceinline__ void epilogue(const AttnParams& p, const Bars& bar, uint32_t tmem, int q, int lane,
+                                         const float* xch) {
+  const int row = q * 32 + lane;
+  const uint32_t tO = tmem + TM_O + (static_cast<uint32_t>(q * 32) << 16);
+  uint32_t zero[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) zero[i] = 0u;
+  int it = 0;
+  int64_t tile = p.tile_begin + blockIdx.x;
+  if (tile < p.n_tiles) {
+#pragma unroll
+    for (int i = 0; i < D / 32; ++i) tmem_st32(tO + i * 32, zero);  // every PV accumulates into O
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar.o_empty);
+  }
+  for (; tile < p.n_tiles; tile += gridDim.x, ++it) {
+    const Tile t = decode_tile(p, tile);
+    const int buf = it & 1;
+    mbar_wait(&bar.stats_full[buf], (it >> 1) & 1);
+    const float mrow = xch[buf * 256 + row], lrow = xch[buf * 256 + 128 + row];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bar.stats_empty[buf]);
+    const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
+    mbar_wait(bar.o_full, it & 1);
+    tc_fence_after();
+    const bool valid = row < t.rows;
+    const int64_t out_row = static_cast<int64_t>(t.row0) + t.q0 + row;
+#pragma unroll 1
+    for (int i = 0; i < D / 32; ++i) {  // 32 columns at a time (this warp's register budget)
+      uint32_t o[32];
+      tmem_ld32(tO + i * 32, o);
+      tmem_ld_wait();
+      tmem_st32(tO + i * 32, zero);  // cleared for the next tile
+      if (valid) store_row32<OUT_F32>(p.out, out_row * D + i * 32, o, inv);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar.o_empty);  // the next tile's PVs may start
+    if (valid && p.lse != nullptr) p.lse[out_row] = lrow > 0.f ? mrow * 0.69314718055994531f + logf(lrow) : -INFINITY;
   }
 }
 
@@ -752,8 +839,12 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     }
     mbar_init(bar.q_full, NSOFT);
     mbar_init(bar.o_full, 2);
-    mbar_init(bar.o_empty, NSOFT);
+    mbar_init(bar.o_empty, FGA_EPI_WARPS ? 4 : NSOFT);
     mbar_init(bar.pv_issued, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar.stats_full[i], NSOFT);
+      mbar_init(&bar.stats_empty[i], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -779,6 +870,8 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     setmaxnreg_dec<REG_OTHER>();
     if (warp < WARP_PROD0) {
       mma_chain<D>(p, smem, bar, tmem, warp - WARP_MMA0);
+    } else if (FGA_EPI_WARPS && warp >= WARP_EPI0) {
+      epilogue<D, OUT_F32>(p, bar, tmem, warp & 3, lane, reinterpret_cast<const float*>(smem + L::OFF_XCH));
     } else if (FGA_PROD_SPLIT) {
       if (warp < WARP_PROD0 + 4)
         producer_half<D>(p, &tmK2, &tmV2, smem, bar, ((warp - WARP_PROD0) >> 1) ^ FGA_PROD_SWAP, (warp - WARP_PROD0) & 1, lane);
