@@ -96,6 +96,9 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 #ifndef FGA_NOGATHER
 #define FGA_NOGATHER 0  // timing experiments only
 #endif
+#ifndef FGA_KEY_PREFETCH
+#define FGA_KEY_PREFETCH 0  // producers load the next chunk's keys while the current chunk is copied
+#endif
 #ifndef FGA_PV_ORDER
 #define FGA_PV_ORDER 1  // PVs issued in chunk order across the two issuers (bitwise-reproducible O)
 #endif
@@ -315,6 +318,7 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
   uint64_t* emptyb = kv ? bar.v_empty : bar.k_empty;
   const CUtensorMap* tm = kv ? tmV2 : tmK2;
   constexpr int PER = 8 / RPI;
+  int knext[ROWS / 32];  // FGA_KEY_PREFETCH: the next chunk's keys
   uint32_t item = 0;
   for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
     const Tile t = decode_tile(p, tile);
@@ -338,7 +342,8 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
 #pragma unroll
       for (int i = 0; i < ROWS / 32; ++i) {
         const int row = c * BN + part * ROWS + i * 32 + lane;
-        keys[i] = row < t.count ? __ldg(t.list + row) : -1;
+        if (FGA_KEY_PREFETCH && c > 0) keys[i] = knext[i];  // loaded while the previous chunk was copied
+        else keys[i] = row < t.count ? __ldg(t.list + row) : -1;
       }
       mbar_wait(&emptyb[slot], (use & 1) ^ 1);
       const char* src = gsrc;
@@ -365,6 +370,13 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
             const char* g = src + static_cast<size_t>(static_cast<uint32_t>(max(key, 0))) * (D * 2);
             cp_async16(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, g, key >= 0 ? 16u : 0u);
           }
+        }
+      }
+      if (FGA_KEY_PREFETCH) {
+#pragma unroll
+        for (int i = 0; i < ROWS / 32; ++i) {
+          const int row = (c + 1) * BN + part * ROWS + i * 32 + lane;
+          knext[i] = row < t.count ? __ldg(t.list + row) : -1;
         }
       }
       cp_async_arrive_noinc(full);
