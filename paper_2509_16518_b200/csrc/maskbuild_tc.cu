@@ -36,7 +36,8 @@ constexpr int CB_EW = 4;              // epilogue warps per TMEM lane quadrant
 constexpr int CB_EPI = 4 * CB_EW;      // epilogue warps 0..15
 constexpr int CB_WARPS = CB_EPI + 2;   // + MMA issuer + TMA producer
 constexpr int CB_NS = 4;  // K ring slots
-constexpr int CB_BARS = 2 + 2 * CB_NS + 4;
+constexpr int CB_SB = 4;  // S buffers in TMEM (4 x 128 columns): the MMA runs up to 3 tiles ahead
+constexpr int CB_BARS = 2 + 2 * CB_NS + 2 * CB_SB;
 
 template <int D>
 struct CbSmem {
@@ -65,8 +66,8 @@ __device__ __forceinline__ CbBars cb_bars(uint8_t* smem) {
   r.k_full = b + 2;
   r.k_empty = r.k_full + CB_NS;
   r.s_full = r.k_empty + CB_NS;
-  r.s_empty = r.s_full + 2;
-  r.tmem_slot = reinterpret_cast<uint32_t*>(r.s_empty + 2);
+  r.s_empty = r.s_full + CB_SB;
+  r.tmem_slot = reinterpret_cast<uint32_t*>(r.s_empty + CB_SB);
   return r;
 }
 
@@ -104,14 +105,14 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       mbar_init(&bar.k_full[i], 1);
       mbar_init(&bar.k_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < CB_SB; ++i) {
       mbar_init(&bar.s_full[i], 1);
       mbar_init(&bar.s_empty[i], CB_EPI);
     }
     fence_barrier_init();
   }
   if (warp == 0) {
-    tmem_alloc(bar.tmem_slot, 256);
+    tmem_alloc(bar.tmem_slot, 128 * CB_SB);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -154,9 +155,9 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
       mbar_wait(bar.q_full, it & 1);
       for (int c = 0; c < nch; ++c, ++kc, ++sc) {
-        const uint32_t slot = kc % CB_NS, use = kc / CB_NS, b = sc & 1;
+        const uint32_t slot = kc % CB_NS, use = kc / CB_NS, b = sc % CB_SB;
         mbar_wait(&bar.k_full[slot], use & 1);
-        mbar_wait(&bar.s_empty[b], ((sc >> 1) & 1) ^ 1);
+        mbar_wait(&bar.s_empty[b], ((sc / CB_SB) & 1) ^ 1);
         tc_fence_after();
         const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
         if (elect_one()) {
@@ -202,8 +203,8 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       float m = -INFINITY;
       double den = 0.0;
       for (int c = 0; c < nch; ++c, ++sc) {
-        const uint32_t b = sc & 1;
-        mbar_wait(&bar.s_full[b], (sc >> 1) & 1);
+        const uint32_t b = sc % CB_SB;
+        mbar_wait(&bar.s_full[b], (sc / CB_SB) & 1);
         tc_fence_after();
         uint32_t v[32];
         tmem_ld32(tl + b * 128, v);
@@ -212,36 +213,32 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar.s_empty[b]);
         if (PASS == 0) {
-          // columns: keys j = c*128 + 32w + k; s = fl(acc * scale) as attention_map's _scores
+          // columns: keys j = c*128 + 32w + k.  The row max is taken on the raw dot products
+          // (scale > 0 and rounding is monotonic, so fl(max(acc) * scale) = max(fl(acc * scale)),
+          // attention_map's s), and each term exp(s - m) is one FFMA2 + MUFU ex2 on
+          // acc * scale * log2e - m * log2e; their rounding errors average out over the row's N
+          // terms, each chunk's 32 summed in fp32, the row in fp64.
           const int jbase = c * BN + w * 32;
-          float s[32];
-          float cmax = -INFINITY;
-          if (jbase + 32 <= p.n) {
+          if (jbase + 32 > p.n) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              s[k] = __fmul_rn(__uint_as_float(v[k]), p.scale);
-              cmax = fmaxf(cmax, s[k]);
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              s[k] = jbase + k < p.n ? __fmul_rn(__uint_as_float(v[k]), p.scale) : -INFINITY;
-              cmax = fmaxf(cmax, s[k]);
-            }
+            for (int k = 0; k < 32; ++k)
+              if (jbase + k >= p.n) v[k] = __float_as_uint(-INFINITY);
           }
+          float amax = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) amax = fmax3f(amax, __uint_as_float(v[k]), __uint_as_float(v[k + 1]));
+          const float cmax = __fmul_rn(amax, p.scale);
           if (cmax > m) {
             den = m == -INFINITY ? 0.0 : den * exp(static_cast<double>(m) - static_cast<double>(cmax));
             m = cmax;
           }
           if (m != -INFINITY) {  // (columns entirely past the sequence end add nothing)
-            // terms exp(s - m) by MUFU ex2 on (s - m) * log2e; their rounding errors average out
-            // over the row's N terms, each chunk's 32 summed in fp32, the row in fp64
-            const float ml = m * 1.4426950408889634f;
+            const float sl = p.scale * 1.4426950408889634f, ml = m * 1.4426950408889634f;
             float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < 32; k += 2) {
-              const float2 x = __ffma2_rn(make_float2(s[k], s[k + 1]), make_float2(1.4426950408889634f, 1.4426950408889634f),
-                                          make_float2(-ml, -ml));
+              const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                                          make_float2(sl, sl), make_float2(-ml, -ml));
               acc = __fadd2_rn(acc, make_float2(ex2(x.x), ex2(x.y)));
             }
             den += static_cast<double>(acc.x) + static_cast<double>(acc.y);
@@ -319,7 +316,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, 128 * CB_SB);
   }
 }
 
