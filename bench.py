@@ -475,6 +475,23 @@ def extras(args, torch, np, fga, _lib, cfg, q, k, v, keep, mask, out, flops, flu
                           "bits_frac": b_bytes / (b_ms * 1e-3) / 1e9 / hbm_peak,
                           "layer_ms_incl_compaction": kernel_ms + min(c_ms, b_ms)}
 
+    # ---- K1a threshold builders on the same Q/K (masks.py:94-150), each to a device mask:
+    #      the cached-threshold builder on the tensor cores (the paper recalibrates it every 15
+    #      denoising iterations) and the avg-query builders
+    from paper_2509_16518_b200 import masks as fmasks
+
+    builders = {}
+    for name, fn in (
+            ("cached_threshold_ms", lambda: fmasks.build_mask_cached_qk(q, k, cfg, 0.5 / n, device_result=True)),
+            ("avg_query_topk_ms", lambda: fmasks.build_mask(q, k, cfg, fmasks.MaskBuilderConfig(
+                "avg_query_topk", top_k=count), device_result=True)),
+            ("avg_query_threshold_ms", lambda: fmasks.build_mask(q, k, cfg, fmasks.MaskBuilderConfig(
+                "avg_query_threshold", tau=1.0 / d), device_result=True))):
+        tb = timed_steps(torch, fn, 3, flush, stream)
+        builders[name] = sorted(tb)[len(tb) // 2]
+    builders["cached_amortised_per_iteration_ms"] = builders["cached_threshold_ms"] / 15
+    line["mask_builders"] = builders
+
     # ---- e2e through the public API from pinned host buffers: H2D of Q/K/V and the
     #      bit-packed slice mask, K1b compaction, attention, D2H of O, overlapped over head slabs
     bits = fga.pack_keep_bits(keep)
