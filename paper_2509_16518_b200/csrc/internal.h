@@ -34,6 +34,8 @@ int launch_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows
                        int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream);
 int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s, int round, float* gmax,
                                float* row_max, cudaStream_t st);
+int launch_pooled_scores_tc(const float* qbar, const void* k, const fga_shape& s, int round, float* scores,
+                            cudaStream_t st);
 int launch_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t n, int32_t* idx,
                    int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream);
 

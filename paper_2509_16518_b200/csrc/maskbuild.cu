@@ -363,6 +363,14 @@ int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int r
   pooled_mean_kernel<<<static_cast<unsigned>(B * H * G), 128, 0, st>>>(
       static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N), static_cast<int>(D), static_cast<int>(M),
       static_cast<int>(G));
+  const char* cc = std::getenv("FGA_POOLED_CC");  // 1: the CUDA-core tile kernel below
+  if (cc == nullptr || cc[0] != '1') {
+    const int rc = launch_pooled_scores_tc(qbar, k, s, round, scores, st);
+    if (rc != FGA_EUNSUPPORTED) {
+      cudaFreeAsync(qbar, st);
+      return rc;
+    }
+  }
   const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
   dim3 grid(static_cast<unsigned>((N + PT - 1) / PT), static_cast<unsigned>((G + PT - 1) / PT),
             static_cast<unsigned>(B * H));

@@ -23,6 +23,7 @@
 // lane quadrant, 32 columns each), 16 MMA issuer, 17 TMA producer (Q tile + 4-slot K ring).
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "attn_common.cuh"
@@ -35,20 +36,24 @@ namespace {
 constexpr int CB_EW = 4;              // epilogue warps per TMEM lane quadrant
 constexpr int CB_EPI = 4 * CB_EW;      // epilogue warps 0..15
 constexpr int CB_WARPS = CB_EPI + 2;   // + MMA issuer + TMA producer
-constexpr int CB_NS = 4;  // K ring slots
+constexpr int cb_nq(int pass) { return pass == 2 ? 3 : 1; }  // Q-side tiles per unit (pass 2: q̄ hi/mid/lo)
+constexpr int cb_ns(int pass) { return pass == 2 ? 3 : 4; }  // K ring slots
+constexpr int CB_NS = 4;                                      // barrier slots (max ring)
 constexpr int CB_SB = 4;  // S buffers in TMEM (4 x 128 columns): the MMA runs up to 3 tiles ahead
 constexpr int CB_BARS = 2 + 2 * CB_NS + 2 * CB_SB;
 
-template <int D>
+template <int D, int PASS>
 struct CbSmem {
   static constexpr int KV = (D / 64) * HALF;  // one 128-row tile
+  static constexpr int NQ = cb_nq(PASS), NS = cb_ns(PASS);
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = KV;
-  static constexpr int OFF_BAR = OFF_K + CB_NS * KV;
+  static constexpr int OFF_K = NQ * KV;
+  static constexpr int OFF_BAR = OFF_K + NS * KV;
   static constexpr int OFF_TAB = OFF_BAR + 256;       // pass 1: (m_i, 1/den_i, m_i + ln den_i) per query
   static constexpr int OFF_XCH = OFF_TAB + 128 * 16;  // pass 0: (m, den) per slice; pass 1: candidates x 2
   static constexpr int BYTES = OFF_XCH + 2 * 3 * CB_EW * 128 * 4;
   static_assert(CB_EW * 128 * 12 <= 2 * 3 * CB_EW * 128 * 4, "exchange area");
+  static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
   static_assert(CB_BARS * 8 + 8 <= 256, "barrier area");
 };
 
@@ -57,9 +62,9 @@ struct CbBars {
   uint32_t* tmem_slot;
 };
 
-template <int D>
+template <int D, int PASS>
 __device__ __forceinline__ CbBars cb_bars(uint8_t* smem) {
-  uint64_t* b = reinterpret_cast<uint64_t*>(smem + CbSmem<D>::OFF_BAR);
+  uint64_t* b = reinterpret_cast<uint64_t*>(smem + CbSmem<D, PASS>::OFF_BAR);
   CbBars r;
   r.q_full = b;
   r.q_empty = b + 1;
@@ -74,7 +79,12 @@ __device__ __forceinline__ CbBars cb_bars(uint8_t* smem) {
 struct CbParams {
   int64_t bh;   // B * H
   int n;        // sequence length
-  int tiles;    // ceil(n / 128): query tiles = groups (M = 128)
+  int tiles;    // units per (b, h): ceil(n / 128) query tiles = groups (passes 0, 1), ceil(G / 128) group tiles (pass 2)
+  int nch;      // key chunks per unit: ceil(n / 128)
+  int groups;   // pass 2: G
+  int64_t part_rows;  // pass 2: rows of one q̄ part (B*H*G)
+  float* scores;      // pass 2: [B*H*G*N]
+  int kslabs;         // pass 2: key ranges per (b*h, group tile)
   float scale;
   int round;
   float* row_max;  // [B*H*N]
@@ -88,20 +98,30 @@ template <int D, int PASS>
 __global__ void __launch_bounds__(32 * CB_WARPS, 1)
     cached_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const CbParams p) {
-  using L = CbSmem<D>;
+  using L = CbSmem<D, PASS>;
   extern __shared__ __align__(1024) uint8_t smem_cb[];
   uint8_t* smem = smem_cb;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
-  const CbBars bar = cb_bars<D>(smem);
+  const CbBars bar = cb_bars<D, PASS>(smem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t n_units = p.bh * p.tiles;
-  const int nch = p.tiles;  // key chunks per unit
+  const int ks_n = PASS == 2 ? p.kslabs : 1;  // pass 2 also splits the keys over units (parallelism)
+  const int64_t n_units = p.bh * p.tiles * ks_n;
+  // unit u -> (b*h, tile t, key chunks [c_lo, c_hi))
+  auto unit = [&](int64_t u, int64_t& bh, int& t, int& c_lo, int& c_hi) {
+    const int ks = static_cast<int>(u % ks_n);
+    const int64_t r = u / ks_n;
+    bh = r / p.tiles;
+    t = static_cast<int>(r % p.tiles);
+    c_lo = static_cast<int>(static_cast<int64_t>(p.nch) * ks / ks_n);
+    c_hi = static_cast<int>(static_cast<int64_t>(p.nch) * (ks + 1) / ks_n);
+  };
+  const int nch = p.nch;  // key chunks per unit
   if (tid == 0) {
     prefetch_tmap(&tmQ);
     prefetch_tmap(&tmK);
     mbar_init(bar.q_full, 1);
     mbar_init(bar.q_empty, 1);
-    for (int i = 0; i < CB_NS; ++i) {
+    for (int i = 0; i < L::NS; ++i) {
       mbar_init(&bar.k_full[i], 1);
       mbar_init(&bar.k_empty[i], 1);
     }
@@ -127,15 +147,21 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       uint32_t kc = 0;
       int it = 0;
       for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-        const int64_t bh = u / p.tiles;
-        const int t = static_cast<int>(u % p.tiles);
+        int64_t bh;
+        int t, c_lo, c_hi;
+        unit(u, bh, t, c_lo, c_hi);
         const int row0 = static_cast<int>(bh * p.n);
         mbar_wait(bar.q_empty, (it & 1) ^ 1);
-        mbar_expect_tx(bar.q_full, BM * D * 2);
+        mbar_expect_tx(bar.q_full, L::NQ * BM * D * 2);
 #pragma unroll
-        for (int h = 0; h < D / 64; ++h) tma_load_2d(smem + L::OFF_Q + h * HALF, &tmQ, bar.q_full, h * 64, row0 + t * BM, pol_q);
-        for (int c = 0; c < nch; ++c, ++kc) {
-          const uint32_t slot = kc % CB_NS, use = kc / CB_NS;
+        for (int qp = 0; qp < L::NQ; ++qp) {
+          const int qrow = PASS == 2 ? static_cast<int>(qp * p.part_rows + bh * p.groups) + t * BM : row0 + t * BM;
+#pragma unroll
+          for (int h = 0; h < D / 64; ++h)
+            tma_load_2d(smem + L::OFF_Q + qp * L::KV + h * HALF, &tmQ, bar.q_full, h * 64, qrow, pol_q);
+        }
+        for (int c = c_lo; c < c_hi; ++c, ++kc) {
+          const uint32_t slot = kc % L::NS, use = kc / L::NS;
           mbar_wait(&bar.k_empty[slot], (use & 1) ^ 1);
           mbar_expect_tx(&bar.k_full[slot], BN * D * 2);
 #pragma unroll
@@ -153,23 +179,31 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
     uint32_t kc = 0, sc = 0;
     int it = 0;
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+      int64_t bh;
+      int t, c_lo, c_hi;
+      unit(u, bh, t, c_lo, c_hi);
       mbar_wait(bar.q_full, it & 1);
-      for (int c = 0; c < nch; ++c, ++kc, ++sc) {
-        const uint32_t slot = kc % CB_NS, use = kc / CB_NS, b = sc % CB_SB;
+      for (int c = c_lo; c < c_hi; ++c, ++kc, ++sc) {
+        const uint32_t slot = kc % L::NS, use = kc / L::NS, b = sc % CB_SB;
         mbar_wait(&bar.k_full[slot], use & 1);
         mbar_wait(&bar.s_empty[b], ((sc / CB_SB) & 1) ^ 1);
         tc_fence_after();
         const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
-            if (PASS == 0) umma_ss(tmem + b * 128, dq0 + off, dk + off, IDESC, kk > 0 ? 1u : 0u);  // S = Q K^T
-            else umma_ss(tmem + b * 128, dk + off, dq0 + off, IDESC, kk > 0 ? 1u : 0u);           // S^T = K Q^T
+          for (int qp = 0; qp < L::NQ; ++qp) {  // pass 2: S^T = K (q̄_hi + q̄_mid + q̄_lo)^T, exact splits
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
+              const uint64_t dq = dq0 + ((qp * L::KV) >> 4) + off;
+              const uint32_t acc = (qp > 0 || kk > 0) ? 1u : 0u;
+              if (PASS == 0) umma_ss(tmem + b * 128, dq, dk + off, IDESC, acc);  // S = Q K^T
+              else umma_ss(tmem + b * 128, dk + off, dq, IDESC, acc);            // S^T = K Q^T
+            }
           }
           umma_commit(&bar.s_full[b]);
           umma_commit(&bar.k_empty[slot]);
-          if (c == nch - 1) umma_commit(bar.q_empty);
+          if (c == c_hi - 1) umma_commit(bar.q_empty);
         }
         __syncwarp();
       }
@@ -183,8 +217,9 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
     const float4* tab = reinterpret_cast<const float4*>(smem + L::OFF_TAB);
     uint32_t sc = 0;
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-      const int64_t bh = u / p.tiles;
-      const int t = static_cast<int>(u % p.tiles);
+      int64_t bh;
+      int t, c_lo, c_hi;
+      unit(u, bh, t, c_lo, c_hi);
       const int64_t row0 = bh * p.n;
       const int q0 = t * BM;
       if (PASS == 1) {
@@ -202,7 +237,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       }
       float m = -INFINITY;
       double den = 0.0;
-      for (int c = 0; c < nch; ++c, ++sc) {
+      for (int c = c_lo; c < c_hi; ++c, ++sc) {
         const uint32_t b = sc % CB_SB;
         mbar_wait(&bar.s_full[b], (sc / CB_SB) & 1);
         tc_fence_after();
@@ -212,7 +247,24 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar.s_empty[b]);
-        if (PASS == 0) {
+        if (PASS == 2) {
+          // row: key j = c*128 + row; columns: groups g = 128t + 32w + k (masks.py:108-118):
+          // s = exp(k_j . q̄_g * scale) / D, bf16-rounded
+          const int j = c * BN + row;
+          constexpr float inv_d = 1.0f / D;  // D is a power of two: x / D == x * (1/D) exactly
+          if (j < p.n) {
+            float* dst = p.scores + (bh * p.groups + t * BM + w * 32) * static_cast<int64_t>(p.n) + j;
+            const int kmax = min(32, p.groups - (t * BM + w * 32));
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              if (k < kmax) {
+                float sc = __fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), p.scale)), inv_d);
+                if (p.round) sc = __bfloat162float(__float2bfloat16_rn(sc));
+                dst[static_cast<int64_t>(k) * p.n] = sc;
+              }
+            }
+          }
+        } else if (PASS == 0) {
           // columns: keys j = c*128 + 32w + k.  The row max is taken on the raw dot products
           // (scale > 0 and rounding is monotonic, so fl(max(acc) * scale) = max(fl(acc * scale)),
           // attention_map's s), and each term exp(s - m) is one FFMA2 + MUFU ex2 on
@@ -323,13 +375,13 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
 template <int D, int PASS>
 int launch_pass(const CUtensorMap* maps, const CbParams& p, cudaStream_t st) {
   auto kern = cached_tc_kernel<D, PASS>;
-  const int smem = CbSmem<D>::BYTES;
+  const int smem = CbSmem<D, PASS>::BYTES;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return check_launch("cudaFuncSetAttribute(cached_tc)");
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t units = p.bh * p.tiles;
+  const int64_t units = p.bh * p.tiles * (PASS == 2 ? p.kslabs : 1);
   kern<<<static_cast<unsigned>(units < sms ? units : sms), 32 * CB_WARPS, smem, st>>>(maps[0], maps[1], p);
   return check_launch("cached_tc_kernel");
 }
@@ -354,6 +406,7 @@ int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s,
   p.bh = B * H;
   p.n = static_cast<int>(N);
   p.tiles = static_cast<int>((N + BM - 1) / BM);
+  p.nch = p.tiles;
   p.scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
   p.round = round;
   p.row_max = row_max;
@@ -362,6 +415,59 @@ int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s,
   rc = D == 64 ? launch_pass<64, 0>(maps, p, st) : launch_pass<128, 0>(maps, p, st);
   if (rc == FGA_OK) rc = D == 64 ? launch_pass<64, 1>(maps, p, st) : launch_pass<128, 1>(maps, p, st);
   cudaFreeAsync(rinv, st);
+  return rc;
+}
+
+// q̄ (fp32) -> three bf16 parts with hi + mid + lo == q̄ exactly (8 + 8 + 8 significand bits),
+// so K q̄^T is three exact-product bf16 MMAs accumulated in fp32.
+__global__ void split3_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ parts, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = x[i];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const float r1 = v - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    parts[i] = hi;
+    parts[n + i] = mid;
+    parts[2 * n + i] = lo;
+  }
+}
+
+// Avg-query scores s[b,h,g,j] = exp(k_j . q̄_g * scale) / D on the tensor cores (pass 2);
+// FGA_EUNSUPPORTED unless D is 64 or 128.  qbar: fp32 [B*H*G, D] (pooled_mean_kernel).
+int launch_pooled_scores_tc(const float* qbar, const void* k, const fga_shape& s, int round, float* scores,
+                            cudaStream_t st) {
+  const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
+  if (D != 64 && D != 128) return FGA_EUNSUPPORTED;
+  const int64_t G = (N + M - 1) / M;
+  const int64_t rows = B * H * N, qrows = B * H * G;
+  if (rows >= (int64_t(1) << 31) || 3 * qrows >= (int64_t(1) << 31)) return FGA_EUNSUPPORTED;
+  __nv_bfloat16* parts = nullptr;
+  if (cudaMallocAsync(&parts, sizeof(__nv_bfloat16) * 3 * qrows * D, st) != cudaSuccess)
+    return check_launch("cudaMallocAsync");
+  split3_kernel<<<static_cast<unsigned>(std::min<int64_t>((qrows * D + 255) / 256, 148 * 16)), 256, 0, st>>>(
+      qbar, parts, qrows * D);
+  int rc = check_launch("split3_kernel");
+  CUtensorMap maps[2];
+  if (rc == FGA_OK) rc = make_tmap_bf16_2d(&maps[0], parts, 3 * qrows, D, 64, BM);
+  if (rc == FGA_OK) rc = make_tmap_bf16_2d(&maps[1], k, rows, D, 64, BN);
+  if (rc == FGA_OK) {
+    CbParams p{};
+    p.bh = B * H;
+    p.n = static_cast<int>(N);
+    p.tiles = static_cast<int>((G + BM - 1) / BM);
+    p.nch = static_cast<int>((N + BN - 1) / BN);
+    p.groups = static_cast<int>(G);
+    p.part_rows = qrows;
+    p.scores = scores;
+    // enough (b*h, group tile, key range) units for every SM, each at least 8 key chunks
+    p.kslabs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(p.nch / 8, (4 * 148 + p.bh * p.tiles - 1) / (p.bh * p.tiles))));
+    p.scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
+    p.round = round;
+    rc = D == 64 ? launch_pass<64, 2>(maps, p, st) : launch_pass<128, 2>(maps, p, st);
+  }
+  cudaFreeAsync(parts, st);
   return rc;
 }
 

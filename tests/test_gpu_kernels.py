@@ -299,6 +299,27 @@ def test_pooled_scores_and_threshold_keep(golden):
     assert (flips <= mism).all()   # a keep bit can only flip where the score itself differs
 
 
+@pytest.mark.parametrize("n,d,h,m", [(1000, 128, 2, 128), (640, 64, 3, 64), (4100, 128, 1, 128)])
+def test_pooled_scores_tensor_cores_vs_oracle(n, d, h, m, monkeypatch):
+    # q̄ split into three exact bf16 parts on the tensor cores (maskbuild_tc.cu pass 2) and the
+    # CUDA-core tiles (FGA_POOLED_CC=1), both against the NumPy restatement of masks.py:108-118
+    b = 1
+    q = oracle.bf16_round(oracle.gaussian((b, h, n, d), 21))
+    k = oracle.bf16_round(oracle.gaussian((b, h, n, d), 22))
+    ref = oracle.pooled_scores(q, k, m, None, "bf16")
+    gc = oracle.num_groups(n, m)
+    qd, kd = to_bf16_dev(q), to_bf16_dev(k)
+    for cc in ("0", "1"):
+        monkeypatch.setenv("FGA_POOLED_CC", cc)
+        s = torch.full((b, h, gc, n), -1.0, device="cuda", dtype=torch.float32)
+        _lib.call("fga_pooled_scores", ptr(qd), ptr(kd), _lib.shape(b, h, n, d, m), 1, ptr(s), stream())
+        torch.cuda.synchronize()
+        got = s.cpu().numpy()
+        mism = got != ref
+        assert mism.mean() < 1e-3, (cc, mism.mean())
+        assert np.abs(got - ref)[mism].max(initial=0) <= np.abs(ref).max() * 2 ** -7, cc
+
+
 def test_topk_keep_matches_reference(golden):
     for name in ("avgq_thr", "avgq_topk_ties"):
         g = golden(name)
