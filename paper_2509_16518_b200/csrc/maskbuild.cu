@@ -193,14 +193,20 @@ __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t prefix = 0, mask = 0;
   int64_t rem = k;
-  for (int pass = 0; pass < 4; ++pass) {
+  int passes = 4;
+  for (int pass = 0; pass < passes; ++pass) {
     const int shift = 24 - 8 * pass;
     for (int b = tid; b < 256; b += TK) hist[b] = 0;
     __syncthreads();
+    uint32_t low = 0;  // pass 0: do the keys carry bits below the top 16 (i.e. not bf16-valued scores)?
     for (int64_t i = tid; i < n; i += TK) {
       const uint32_t key = keys(row, n, i);
+      if (pass == 0) low |= ((key & 0x80000000u) ? key : ~key) & 0xFFFFu;
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
+    // bf16-valued rows (the builders' rounded scores): two keys with equal top 16 bits are
+    // equal, so two 8-bit passes decide the k-th largest key exactly
+    if (pass == 0 && !__syncthreads_or(low != 0)) passes = 2;
     __syncthreads();
     if (tid == 0) {
       int64_t cum = 0;
@@ -218,6 +224,7 @@ __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t 
     mask |= 255u << shift;
     __syncthreads();
   }
+  if (passes == 2) prefix |= (prefix & 0x80000000u) ? 0u : 0xFFFFu;  // the low half every such key has
   // prefix is the k-th largest key; keep all larger keys and the first `rem` equal ones.
   int64_t taken = 0;
   for (int64_t base = 0; base < n; base += TK) {
