@@ -96,6 +96,9 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 #ifndef FGA_NOGATHER
 #define FGA_NOGATHER 0  // timing experiments only
 #endif
+#ifndef FGA_Q_PREFETCH
+#define FGA_Q_PREFETCH 0  // softmax threads prefetch the next tile's Q rows into L2
+#endif
 #ifndef FGA_KEY_PREFETCH
 #define FGA_KEY_PREFETCH 0  // producers load the next chunk's keys while the current chunk is copied
 #endif
@@ -577,6 +580,17 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
   }
   for (; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
+    if (FGA_Q_PREFETCH && tile + gridDim.x < p.n_tiles) {
+      // the next tile's Q rows -> L2 now, so write_q at the end of this tile reads L2, not HBM
+      // (one 128-byte line per thread: 128 rows x 2D bytes)
+      const Tile nt = decode_tile(p, tile + gridDim.x);
+      const int line = tid, lines_per_row = D / 64;
+      if (line < 128 * lines_per_row) {
+        const char* a = static_cast<const char*>(qptr) +
+                        ((static_cast<int64_t>(nt.row0) + nt.q0 + line / lines_per_row) * D) * 2 + (line % lines_per_row) * 128;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
     float m_use[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};  // l_run: this thread's partial sums
     uint32_t sv[2][32];  // [column half][4k + 2*row + e]: rows r0/r0+8, col 64*half + 8k + 2a + e
     bool have_s = false;  // sv is already loading S_j (issued at the end of the previous chunk)
