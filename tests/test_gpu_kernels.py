@@ -235,6 +235,19 @@ def test_online_rescale_large_dynamic_range(d, order, gain, attn_kernel):
         assert np.abs(lse[bb, hh, lo:hi] - ref_l).max() < 2e-2
 
 
+@pytest.mark.parametrize("b,h,n,d", [(2, 3, 700, 128), (3, 2, 257, 64)])
+def test_batched_heads(b, h, n, d, attn_kernel):
+    # B > 1: tiles are numbered ((b*H + h)*G + g); every (b, h) reads only its own K/V rows
+    m = 128
+    rng = np.random.default_rng(b * 10 + d)
+    q, k, v = (oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32)) for _ in range(3))
+    lists = oracle.random_lists(b, h, n, m, 0.35, seed=b + d)
+    ref = oracle.masked_attention(q, k, v, lists, m)
+    idx, cnt = padded_dev(lists, b, h, n, m)
+    o, _ = run_sparse(to_bf16_dev(q), to_bf16_dev(k), to_bf16_dev(v), idx, cnt, b, h, n, d, m)
+    assert np.abs(o.cpu().numpy() - ref).max() <= ATOL
+
+
 @pytest.mark.parametrize("m", [16, 64, 200, 256])
 def test_group_sizes(m, attn_kernel):
     b, h, n, d = 1, 2, 600, 64
