@@ -181,39 +181,66 @@ struct HashKeys {
 constexpr int TK = 512;
 
 // Keep the k largest keys of each row; among keys equal to the k-th largest,
-// keep the ones with the smallest indices.  4 radix-select passes + 1 ordered pass.
+// keep the ones with the smallest indices.  Radix select on the 32-bit ordered keys with
+// digits of 12 + 12 + 8 bits (12 + 4 for rows of bf16-valued scores, detected in the first
+// pass: two keys with equal top 16 bits are then equal), then one ordered pass.  The wide
+// first digit spreads rows whose values share a few exponents (the builders' scores) over
+// many histogram bins instead of serialising their atomics on two or three.
+constexpr int TK_BINS = 4096;
 template <typename Keys>
 __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t k, uint8_t* __restrict__ keep) {
-  __shared__ uint32_t hist[256];
+  __shared__ uint32_t hist[TK_BINS];
   __shared__ uint32_t s_prefix;
   __shared__ int64_t s_rem;
+  __shared__ int64_t s_wsum[TK / 32];
   __shared__ int s_warp[TK / 32];
   __shared__ int s_tot;
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t prefix = 0, mask = 0;
   int64_t rem = k;
-  int passes = 4;
-  for (int pass = 0; pass < passes; ++pass) {
-    const int shift = 24 - 8 * pass;
-    for (int b = tid; b < 256; b += TK) hist[b] = 0;
+  int shift = 32;
+  bool bf16_row = false;
+  for (int pass = 0; shift > (bf16_row ? 16 : 0); ++pass) {
+    const int width = pass == 0 ? 12 : bf16_row ? 4 : (shift > 8 ? 12 : 8);
+    shift -= width;
+    const int nb = 1 << width;
+    for (int b = tid; b < nb; b += TK) hist[b] = 0;
     __syncthreads();
-    uint32_t low = 0;  // pass 0: do the keys carry bits below the top 16 (i.e. not bf16-valued scores)?
+    uint32_t low = 0;
     for (int64_t i = tid; i < n; i += TK) {
       const uint32_t key = keys(row, n, i);
       if (pass == 0) low |= ((key & 0x80000000u) ? key : ~key) & 0xFFFFu;
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & (nb - 1)], 1u);
     }
-    // bf16-valued rows (the builders' rounded scores): two keys with equal top 16 bits are
-    // equal, so two 8-bit passes decide the k-th largest key exactly
-    if (pass == 0 && !__syncthreads_or(low != 0)) passes = 2;
+    if (pass == 0) bf16_row = !__syncthreads_or(low != 0);
     __syncthreads();
-    if (tid == 0) {
-      int64_t cum = 0;
-      int b = 255;
-      for (; b > 0; --b) {
-        if (cum + hist[b] >= rem) break;
-        cum += hist[b];
+    // the digit b with  sum_{d > b} hist[d] < rem <= sum_{d >= b} hist[d]: thread t owns the 8 bins
+    // nb-1-8t .. nb-8-8t (descending); a block scan of the segment sums finds the owner
+    const int nseg = nb / 8;
+    int64_t own = 0;
+    if (tid < nseg) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) own += hist[nb - 1 - 8 * tid - e];
+    }
+    int64_t incl = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    int64_t before = 0;
+    for (int w = 0; w < warp; ++w) before += s_wsum[w];
+    const int64_t excl = before + incl - own;
+    if (tid < nseg && excl < rem && rem <= excl + own) {
+      int64_t cum = excl;
+      int b = nb - 1 - 8 * tid;
+      for (int e = 0; e < 7; ++e, --b) {
+        const uint32_t hb = hist[b];
+        if (cum + hb >= rem) break;
+        cum += hb;
       }
       s_prefix = prefix | (static_cast<uint32_t>(b) << shift);
       s_rem = rem - cum;
@@ -221,10 +248,10 @@ __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t 
     __syncthreads();
     prefix = s_prefix;
     rem = s_rem;
-    mask |= 255u << shift;
+    mask |= static_cast<uint32_t>(nb - 1) << shift;
     __syncthreads();
   }
-  if (passes == 2) prefix |= (prefix & 0x80000000u) ? 0u : 0xFFFFu;  // the low half every such key has
+  if (bf16_row) prefix |= (prefix & 0x80000000u) ? 0u : 0xFFFFu;  // the low half every such key has
   // prefix is the k-th largest key; keep all larger keys and the first `rem` equal ones.
   int64_t taken = 0;
   for (int64_t base = 0; base < n; base += TK) {

@@ -6,5 +6,5 @@ import csv
 rows=list(csv.reader(open("/tmp/ncu_k.csv")))
 h=rows[0]
 for r in rows[1:]:
-    if len(r)==len(h) and "fga" in r[h.index("Kernel Name")]: print(r[h.index("Kernel Name")][:60], r[h.index("Metric Value")])
+    if len(r)==len(h) and ("fga" in r[h.index("Kernel Name")] or "unnamed" in r[h.index("Kernel Name")]): print(r[h.index("Kernel Name")][:60], r[h.index("Metric Value")])
 PY
