@@ -187,6 +187,10 @@ constexpr int TK = 512;
 // first digit spreads rows whose values share a few exponents (the builders' scores) over
 // many histogram bins instead of serialising their atomics on two or three.
 constexpr int TK_BINS = 4096;
+#ifndef FGA_TOPK_EQ_MAX
+#define FGA_TOPK_EQ_MAX 256
+#endif
+constexpr int TK_EQ_MAX = FGA_TOPK_EQ_MAX > 0 ? FGA_TOPK_EQ_MAX : 1;  // ties at the threshold resolved by rank counting up to this many
 template <typename Keys>
 __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t k, uint8_t* __restrict__ keep) {
   __shared__ uint32_t hist[TK_BINS];
@@ -195,6 +199,8 @@ __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t 
   __shared__ int64_t s_wsum[TK / 32];
   __shared__ int s_warp[TK / 32];
   __shared__ int s_tot;
+  __shared__ int64_t s_eqcnt;
+  __shared__ int s_eqidx[TK_EQ_MAX];
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t prefix = 0, mask = 0;
@@ -244,6 +250,7 @@ __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t 
       }
       s_prefix = prefix | (static_cast<uint32_t>(b) << shift);
       s_rem = rem - cum;
+      s_eqcnt = hist[b];  // after the last digit: the keys equal to the k-th largest
     }
     __syncthreads();
     prefix = s_prefix;
@@ -253,6 +260,29 @@ __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t 
   }
   if (bf16_row) prefix |= (prefix & 0x80000000u) ? 0u : 0xFFFFu;  // the low half every such key has
   // prefix is the k-th largest key; keep all larger keys and the first `rem` equal ones.
+  const int64_t n_eq = s_eqcnt;  // keys equal to prefix
+  if (rem == n_eq) {  // every equal key is kept: no order needed
+    for (int64_t i = tid; i < n; i += TK) keep[row * n + i] = keys(row, n, i) >= prefix ? 1 : 0;
+    return;
+  }
+  if (FGA_TOPK_EQ_MAX > 0 && n_eq <= TK_EQ_MAX) {
+    // few ties: decide the rest in parallel, list the tied indices, keep the rem smallest of them
+    if (tid == 0) s_tot = 0;
+    __syncthreads();
+    for (int64_t i = tid; i < n; i += TK) {
+      const uint32_t key = keys(row, n, i);
+      keep[row * n + i] = key > prefix ? 1 : 0;
+      if (key == prefix) s_eqidx[atomicAdd(&s_tot, 1)] = static_cast<int>(i);
+    }
+    __syncthreads();
+    for (int e = tid; e < n_eq; e += TK) {
+      const int me = s_eqidx[e];
+      int rank = 0;
+      for (int f = 0; f < n_eq; ++f) rank += s_eqidx[f] < me;
+      if (rank < rem) keep[row * n + me] = 1;
+    }
+    return;
+  }
   int64_t taken = 0;
   for (int64_t base = 0; base < n; base += TK) {
     const int64_t i = base + tid;
