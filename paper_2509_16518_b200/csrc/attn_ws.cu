@@ -96,6 +96,9 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 #ifndef FGA_NOGATHER
 #define FGA_NOGATHER 0  // timing experiments only
 #endif
+#ifndef FGA_TMA_ELECT
+#define FGA_TMA_ELECT 0  // balanced producers gather by TMA tile::gather4 from one elected lane
+#endif
 #ifndef FGA_Q_PREFETCH
 #define FGA_Q_PREFETCH 0  // softmax threads prefetch the next tile's Q rows into L2
 #endif
@@ -305,7 +308,8 @@ __device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap*
 // each warp sees every use of every slot of its ring and the empty parity stays exact.
 template <int D>
 __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
-                                              uint8_t* smem, const Bars& bar, int kv, int part, int lane) {
+                                              const CUtensorMap* tmKg, const CUtensorMap* tmVg, uint8_t* smem,
+                                              const Bars& bar, int kv, int part, int lane) {
   using L = WsSmem<D>;
   constexpr int LPR = D / 8;     // lanes per 2*D-byte row
   constexpr int RPI = 32 / LPR;  // rows per warp instruction
@@ -347,6 +351,32 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
         const int row = c * BN + part * ROWS + i * 32 + lane;
         if (FGA_KEY_PREFETCH && c > 0) keys[i] = knext[i];  // loaded while the previous chunk was copied
         else keys[i] = row < t.count ? __ldg(t.list + row) : -1;
+      }
+      if (FGA_TMA_ELECT) {
+        // TMA tile::gather4 issued by one elected lane: 16 gather4 x D/64 column blocks for
+        // the 64 rows; rows past the list end repeat the chunk's first key (masked to -inf)
+        const CUtensorMap* tmg = kv ? tmVg : tmKg;
+        const int first = __shfl_sync(0xffffffffu, keys[0], 0);  // row part*64 (< count: chunk non-empty)
+        mbar_wait(&emptyb[slot], (use & 1) ^ 1);
+        if (lane == 0) mbar_expect_tx(full, ROWS * D * 2);
+#pragma unroll 4
+        for (int g = 0; g < ROWS / 4; ++g) {
+          int rk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = 4 * g + e;
+            const int key = __shfl_sync(0xffffffffu, keys[r >> 5], r & 31);
+            rk[e] = t.row0 + (key >= 0 ? key : max(first, 0));
+          }
+          if (elect_one()) {
+#pragma unroll
+            for (int h = 0; h < D / 64; ++h)
+              tma_gather4(ring + slot * L::KV + h * HALF + (part * ROWS + 4 * g) * 128, tmg, full, h * 64, rk[0], rk[1],
+                          rk[2], rk[3], pol_kv);
+          }
+          __syncwarp();
+        }
+        continue;  // lane 0's arrive.expect_tx is this half's arrival
       }
       mbar_wait(&emptyb[slot], (use & 1) ^ 1);
       const char* src = gsrc;
@@ -842,14 +872,15 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     if (p.dense) {
       prefetch_tmap(&tmK2);
       prefetch_tmap(&tmV2);
-    } else if (FGA_TMA_GATHER != 0) {
+    } else if (FGA_TMA_GATHER != 0 || FGA_TMA_ELECT) {
       prefetch_tmap(&tmKg);
       prefetch_tmap(&tmVg);
     }
     // a chunk completes with 32 cp.async arrivals (LDGSTS producer, dense path: lane 0's
     // expect_tx + 31 arrivals) or with lane 0's expect_tx alone (gather4 producer)
-    const uint32_t k_count = FGA_PROD_SPLIT ? 64u : ((FGA_TMA_GATHER & 1) && !p.dense) ? 1u : 32u;
-    const uint32_t v_count = FGA_PROD_SPLIT ? 64u : ((FGA_TMA_GATHER & 2) && !p.dense) ? 1u : 32u;
+    const uint32_t split_count = (FGA_TMA_ELECT && !p.dense) ? 2u : 64u;
+    const uint32_t k_count = FGA_PROD_SPLIT ? split_count : ((FGA_TMA_GATHER & 1) && !p.dense) ? 1u : 32u;
+    const uint32_t v_count = FGA_PROD_SPLIT ? split_count : ((FGA_TMA_GATHER & 2) && !p.dense) ? 1u : 32u;
     for (int i = 0; i < L::NSK; ++i) {
       mbar_init(&bar.k_full[i], k_count);  // one producer warp per chunk
       mbar_init(&bar.k_empty[i], 1);
@@ -900,7 +931,8 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
       epilogue<D, OUT_F32>(p, bar, tmem, warp & 3, lane, reinterpret_cast<const float*>(smem + L::OFF_XCH));
     } else if (FGA_PROD_SPLIT) {
       if (warp < WARP_PROD0 + 4)
-        producer_half<D>(p, &tmK2, &tmV2, smem, bar, ((warp - WARP_PROD0) >> 1) ^ FGA_PROD_SWAP, (warp - WARP_PROD0) & 1, lane);
+        producer_half<D>(p, &tmK2, &tmV2, &tmKg, &tmVg, smem, bar, ((warp - WARP_PROD0) >> 1) ^ FGA_PROD_SWAP,
+                         (warp - WARP_PROD0) & 1, lane);
     } else if (warp < WARP_PROD0 + NPK) {
       producer<D>(p, &tmK2, &tmV2, &tmKg, &tmVg, smem, bar, 0, warp - WARP_PROD0, NPK, lane);
     } else if (warp < WARP_PROD0 + NPK + NPV) {
