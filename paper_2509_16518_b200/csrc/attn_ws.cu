@@ -96,6 +96,9 @@ constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the
 #ifndef FGA_NOGATHER
 #define FGA_NOGATHER 0  // timing experiments only
 #endif
+#ifndef FGA_TMA_MIX
+#define FGA_TMA_MIX 0  // leading rows of each 64-row half gathered by TMA (multiple of 4; rest cp.async)
+#endif
 #ifndef FGA_TMA_ELECT
 #define FGA_TMA_ELECT 0  // balanced producers gather by TMA tile::gather4 from one elected lane
 #endif
@@ -386,15 +389,36 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
       for (int u = 0; u < PER; ++u)
         dstb[u] = ring_base + slot * L::KV + lane_off + sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
       if (c * BN + part * ROWS + ROWS <= t.count) {
+        if (FGA_TMA_MIX > 0) {
+          // the first FGA_TMA_MIX rows of this half by TMA tile::gather4 from one lane (off the MIO
+          // queue the LDGSTS share with the softmax's MUFU), the rest by cp.async below
+          const CUtensorMap* tmg = kv ? tmVg : tmKg;
+          if (lane == 0) mbar_expect_tx(full, FGA_TMA_MIX * D * 2);
+#pragma unroll
+          for (int g = 0; g < FGA_TMA_MIX / 4; ++g) {
+            int rk[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) rk[e] = t.row0 + __shfl_sync(0xffffffffu, keys[0], 4 * g + e);
+            if (elect_one()) {
+#pragma unroll
+              for (int h = 0; h < D / 64; ++h)
+                tma_gather4(ring + slot * L::KV + h * HALF + (part * ROWS + 4 * g) * 128, tmg, full, h * 64, rk[0],
+                            rk[1], rk[2], rk[3], pol_kv);
+            }
+            __syncwarp();
+          }
+        }
 #pragma unroll
         for (int i = 0; i < ROWS / 32; ++i) {
 #pragma unroll
           for (int mm = 0; mm < 32 / RPI; ++mm) {
+            if (i * 32 + mm * RPI + RPI <= FGA_TMA_MIX) continue;  // (compile-time) rows gathered by TMA
             const uint32_t key = static_cast<uint32_t>(__shfl_sync(0xffffffffu, keys[i], mm * RPI + sub));
             cp_async16_full(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, src + static_cast<size_t>(key) * (D * 2));
           }
         }
       } else {
+        if (FGA_TMA_MIX > 0 && lane == 0) mbar_arrive(full);  // the arrival the TMA part makes in full chunks
 #pragma unroll
         for (int i = 0; i < ROWS / 32; ++i) {
 #pragma unroll
@@ -872,13 +896,13 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     if (p.dense) {
       prefetch_tmap(&tmK2);
       prefetch_tmap(&tmV2);
-    } else if (FGA_TMA_GATHER != 0 || FGA_TMA_ELECT) {
+    } else if (FGA_TMA_GATHER != 0 || FGA_TMA_ELECT || FGA_TMA_MIX > 0) {
       prefetch_tmap(&tmKg);
       prefetch_tmap(&tmVg);
     }
     // a chunk completes with 32 cp.async arrivals (LDGSTS producer, dense path: lane 0's
     // expect_tx + 31 arrivals) or with lane 0's expect_tx alone (gather4 producer)
-    const uint32_t split_count = (FGA_TMA_ELECT && !p.dense) ? 2u : 64u;
+    const uint32_t split_count = (FGA_TMA_ELECT && !p.dense) ? 2u : (FGA_TMA_MIX > 0 && !p.dense) ? 66u : 64u;
     const uint32_t k_count = FGA_PROD_SPLIT ? split_count : ((FGA_TMA_GATHER & 1) && !p.dense) ? 1u : 32u;
     const uint32_t v_count = FGA_PROD_SPLIT ? split_count : ((FGA_TMA_GATHER & 2) && !p.dense) ? 1u : 32u;
     for (int i = 0; i < L::NSK; ++i) {
