@@ -23,14 +23,18 @@
 // Warps (16, one CTA per SM, persistent over tiles strided by the grid):
 //   0-7   softmax + epilogue (+ writing the next tile's Q into TMEM)
 //   8, 9  MMA issuers, one per S/P buffer (chunks of CTA-wide parity 0 / 1)
-//   10-13 gather producers (FGA_PROD_SPLIT, default): K rows 0-63, K rows 64-127,
-//         V rows 0-63, V rows 64-127 of every chunk, one warp per SM sub-partition,
-//         16-byte cp.async into the 128B-swizzled ring slots (3 K + 3 V)
-//   14, 15 idle (FGA_PROD_SPLIT=0: 10-15 are one producer warp per ring slot)
+//   10-13 gather producers: K rows 0-63, K rows 64-127, V rows 0-63, V rows 64-127 of
+//         every chunk, one warp per SM sub-partition, 16-byte cp.async into the
+//         128B-swizzled ring slots (3 K + 3 V)
+//   14, 15 idle
 // TMEM (512 cols): O [0, D) | Q [128, 128 + D/2) | S0 [256, 384) | S1 [384, 512).
 // P_j (bf16 pairs) overwrites S[j%2] cols 0..63.
 // Lazy rescale: the running max used for exp only moves when the row max grows
 // by more than 8 (log2 units); O rows in TMEM are rescaled only then (rarely).
+//
+// Variants measured against this kernel and not kept (TMA gather4 producers, dedicated
+// epilogue warps, S prefetch, FMA-pipe exp2, ...) are listed in DESIGN.md section 4; their
+// code is in the git history (e.g. commit 3cb3ba1).
 #include <cuda_bf16.h>
 
 #include <cmath>
@@ -43,125 +47,53 @@
 namespace fga {
 namespace {
 
-constexpr int NSOFT = 8;        // softmax warps
-constexpr int WARP_MMA0 = 8;    // MMA issuers 8 (buffer 0) and 9 (buffer 1)
+constexpr int NSOFT = 8;      // softmax warps
+constexpr int WARP_MMA0 = 8;  // MMA issuers 8 (buffer 0) and 9 (buffer 1)
 constexpr int WARP_PROD0 = 10;
-constexpr int NPK = 3;          // producer warps of the K ring = its slots (one warp per slot)
-constexpr int NPV = 3;          // producer warps of the V ring = its slots
-#ifndef FGA_EPI_WARPS
-#define FGA_EPI_WARPS 0  // 1: four dedicated epilogue warps (16-19) finish each tile off the softmax's path (measured slower: any 20-warp build is)
-#endif
-#ifndef FGA_NW20
-#define FGA_NW20 0  // timing experiment: 20 warps (register split of the epilogue build) without the role
-#endif
-constexpr bool kWide = FGA_EPI_WARPS || FGA_NW20;
-constexpr int NWARPS = kWide ? 20 : 16;
-constexpr int WARP_EPI0 = 16;
-#ifndef FGA_REG_SOFTMAX
-#define FGA_REG_SOFTMAX (kWide ? 144 : 184)
-#endif
-#ifndef FGA_REG_OTHER
-#define FGA_REG_OTHER (kWide ? 64 : 72)
-#endif
-constexpr int REG_SOFTMAX = FGA_REG_SOFTMAX;
-constexpr int REG_OTHER = FGA_REG_OTHER;
+constexpr int NPROD = 4;      // gather producers 10-13
+constexpr int NWARPS = 16;
+constexpr int REG_SOFTMAX = 184;
+constexpr int REG_OTHER = 72;  // producers and issuers: measured 13% slower at 64
+constexpr int NSK = 3, NSV = 3;  // K / V ring slots
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units (factor 256)
 constexpr float RESCALE_SUM = 256.0f;      // 2^RESCALE_THRESHOLD
 constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
-#ifndef FGA_POLY_EVERY
-#define FGA_POLY_EVERY (1 << 20)
-#endif
-constexpr int POLY_EVERY = FGA_POLY_EVERY;  // 1 in POLY_EVERY exp2 pairs on the FMA pipe (MUFU relief)
-#ifndef FGA_SPLIT_ST
-#define FGA_SPLIT_ST 0
-#endif
-#ifndef FGA_TMA_GATHER
-#define FGA_TMA_GATHER 0  // bit 0: K rows, bit 1: V rows by TMA tile::gather4 (else 16-byte cp.async)
-#endif
-#ifndef FGA_PROD_SPLIT
-#define FGA_PROD_SPLIT 1  // 1: four producer warps, one per sub-partition, half a chunk each
-#endif
-#ifndef FGA_NSK
-#define FGA_NSK 3  // K ring slots (FGA_PROD_SPLIT)
-#endif
-#ifndef FGA_NSV
-#define FGA_NSV 3  // V ring slots (FGA_PROD_SPLIT)
-#endif
-#ifndef FGA_PROD_SWAP
-#define FGA_PROD_SWAP 0  // FGA_PROD_SPLIT: 1 puts the V halves on sub-partitions 2, 3 and K on 0, 1
-#endif
-#ifndef FGA_PREFETCH_S
-#define FGA_PREFETCH_S 0
-#endif
+// Timing-experiment builds (DESIGN.md section 4 "structural floors"); all 0 in production.
 #ifndef FGA_NOGATHER
-#define FGA_NOGATHER 0  // timing experiments only
-#endif
-#ifndef FGA_TMA_MIX
-#define FGA_TMA_MIX 0  // leading rows of each 64-row half gathered by TMA (multiple of 4; rest cp.async)
-#endif
-#ifndef FGA_TMA_ELECT
-#define FGA_TMA_ELECT 0  // balanced producers gather by TMA tile::gather4 from one elected lane
-#endif
-#ifndef FGA_Q_PREFETCH
-#define FGA_Q_PREFETCH 0  // softmax threads prefetch the next tile's Q rows into L2
-#endif
-#ifndef FGA_KEY_PREFETCH
-#define FGA_KEY_PREFETCH 0  // producers load the next chunk's keys while the current chunk is copied
-#endif
-#ifndef FGA_PV_ORDER
-#define FGA_PV_ORDER 1  // PVs issued in chunk order across the two issuers (bitwise-reproducible O)
+#define FGA_NOGATHER 0  // producers copy nothing
 #endif
 #ifndef FGA_NOMMA
-#define FGA_NOMMA 0  // timing experiments only
+#define FGA_NOMMA 0  // issuers commit without MMAs
 #endif
 #ifndef FGA_NOEXP
-#define FGA_NOEXP 0  // timing experiments only
-#endif
-#ifndef FGA_POLY_DEG
-#define FGA_POLY_DEG 3
-#endif
-#ifndef FGA_EXP_SKIP
-#define FGA_EXP_SKIP 0  // timing experiments only
-#endif
-#ifndef FGA_EXP_H2
-#define FGA_EXP_H2 0
+#define FGA_NOEXP 0  // P = S bits, no exp
 #endif
 
 template <int D>
 struct WsSmem {
-  static constexpr int KV = (D / 64) * HALF;       // one K or V chunk
-  // K / V ring slots: one per producer warp (FGA_PROD_SPLIT=0), or any count up to what SMEM holds
-  static constexpr int NSK = FGA_PROD_SPLIT ? FGA_NSK : NPK;
-  static constexpr int NSV = FGA_PROD_SPLIT ? FGA_NSV : NPV;
+  static constexpr int KV = (D / 64) * HALF;  // one K or V chunk
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + NSK * KV;
   static constexpr int OFF_BAR = OFF_V + NSV * KV;
-  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3 + 1 + 4;
-  static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row, x2 tiles
-  static constexpr int BYTES = OFF_XCH + 2 * 2 * 128 * 4;
-  // The two issuers free a ring's slots in chunk order only up to swaps of neighbouring
-  // chunks (c and c+1 come from different issuers).  With one producer warp per slot a
-  // producer waits only for its own slot's previous use, which it issued itself after the
-  // use before had been freed, so the empty-barrier parity can never be two phases behind.
-  static_assert(FGA_PROD_SPLIT || (NPK == NSK && NPV == NSV), "one producer warp per ring slot");
+  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3 + 1;
+  static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row
+  static constexpr int BYTES = OFF_XCH + 2 * 128 * 4;
   static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
-  static_assert(WARP_PROD0 + NPK + NPV <= NWARPS, "too many producer warps");
+  static_assert(WARP_PROD0 + NPROD <= NWARPS, "too many producer warps");
 };
 
 struct Bars {
-  uint64_t* k_full;    // [NSK] count 32 (one producer warp)
-  uint64_t* k_empty;   // [NSK] S-issuer commit
-  uint64_t* v_full;    // [NSV]
-  uint64_t* v_empty;   // [NSV] PV-issuer commit
-  uint64_t* s_full;    // [2]
-  uint64_t* p_full;    // [2] count 8 (every softmax warp)
-  uint64_t* pv_done;   // [2] completion of PV into S buffer b's P
-  uint64_t* pv_issued; // count 1: PV_c has been issued (PVs enter the tensor pipe in chunk order)
-  uint64_t* stats_full;   // [2] count 8: the softmax warps published (m, l) of tile it (buffer it % 2)
-  uint64_t* stats_empty;  // [2] count 4: the epilogue warps read them
-  uint64_t* q_full;    // count 8 (every softmax warp writes a part of Q)
+  uint64_t* k_full;     // [NSK] count 64 (two producer warps x 32 cp.async arrivals)
+  uint64_t* k_empty;    // [NSK] S-issuer commit
+  uint64_t* v_full;     // [NSV] count 64
+  uint64_t* v_empty;    // [NSV] PV-issuer commit
+  uint64_t* s_full;     // [2]
+  uint64_t* p_full;     // [2] count 8 (every softmax warp)
+  uint64_t* pv_done;    // [2] completion of PV into S buffer b's P
+  uint64_t* pv_issued;  // count 1: PV_c has been issued (PVs enter the tensor pipe in chunk order)
+  uint64_t* q_full;     // count 8 (every softmax warp writes a part of Q)
   uint64_t* o_full;
-  uint64_t* o_empty;   // count 8
+  uint64_t* o_empty;    // count 8
   uint32_t* tmem_slot;
 };
 
@@ -171,153 +103,39 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   uint64_t* b = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
   Bars r;
   r.k_full = b;
-  r.k_empty = r.k_full + L::NSK;
-  r.v_full = r.k_empty + L::NSK;
-  r.v_empty = r.v_full + L::NSV;
-  r.s_full = r.v_empty + L::NSV;
+  r.k_empty = r.k_full + NSK;
+  r.v_full = r.k_empty + NSK;
+  r.v_empty = r.v_full + NSV;
+  r.s_full = r.v_empty + NSV;
   r.p_full = r.s_full + 2;
   r.pv_done = r.p_full + 2;
   r.q_full = r.pv_done + 2;
   r.o_full = r.q_full + 1;
   r.o_empty = r.o_full + 1;
   r.pv_issued = r.o_empty + 1;
-  r.stats_full = r.pv_issued + 1;
-  r.stats_empty = r.stats_full + 2;
-  r.tmem_slot = reinterpret_cast<uint32_t*>(r.stats_empty + 2);
+  r.tmem_slot = reinterpret_cast<uint32_t*>(r.pv_issued + 1);
   return r;
 }
 
 // ------------------------------------------------------------------ producers
-// Two rings, each filled and drained in chunk order: ring kv = 0 holds K chunks
-// (freed by the S issuer), ring kv = 1 holds V chunks (freed by the PV issuer).
-// Producer warp w of a ring owns slot w and packs the ring's chunks w, w+npr, ... (CTA-wide
-// chunk order).  Each lane holds 4 of the chunk's 128 keys (loaded before the
-// slot wait); one warp instruction copies RPI rows (LPR lanes x 16 B per row).
-// Rows past the list end are zero-filled (src-size 0), so no stale or NaN bytes
-// reach the MMA.
-template <int D>
-__device__ __forceinline__ void producer(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
-                                         const CUtensorMap* tmKg, const CUtensorMap* tmVg, uint8_t* smem,
-                                         const Bars& bar, int kv, int pw, int npr, int lane) {
-  using L = WsSmem<D>;
-  constexpr int LPR = D / 8;     // lanes per 2*D-byte row
-  constexpr int RPI = 32 / LPR;  // rows per warp instruction
-  const int nslot = kv ? L::NSV : L::NSK;
-  const uint64_t pol_kv = policy_evict_last();
-  const int sub = lane / LPR, ch = lane % LPR;
-  const uint32_t lane_off = static_cast<uint32_t>((ch >> 3) * HALF);
-  const int cc = ch & 7;
-  uint8_t* ring = smem + (kv ? L::OFF_V : L::OFF_K);
-  const uint32_t ring_base = smem_u32(ring);
-  uint64_t* fullb = kv ? bar.v_full : bar.k_full;
-  uint64_t* emptyb = kv ? bar.v_empty : bar.k_empty;
-  const CUtensorMap* tm = kv ? tmV2 : tmK2;
-  const CUtensorMap* tmg = kv ? tmVg : tmKg;
-  uint32_t base = 0;  // CTA-wide index of the tile's first chunk
-  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-    const Tile t = decode_tile(p, tile);
-    const uint32_t n = static_cast<uint32_t>(t.nchunks);
-    const char* gsrc = static_cast<const char*>(kv ? p.v : p.k) + static_cast<int64_t>(t.row0) * (D * 2) + ch * 16;
-    for (uint32_t item = base + (static_cast<uint32_t>(pw) + npr - base % npr) % npr; item < base + n; item += npr) {
-      const int c = static_cast<int>(item - base);
-      const uint32_t slot = item % nslot, use = item / nslot;
-      uint64_t* full = &fullb[slot];
-      if (p.dense) {
-        mbar_wait(&emptyb[slot], (use & 1) ^ 1);
-        if (lane == 0) {
-          mbar_expect_tx(full, BN * D * 2);
-#pragma unroll
-          for (int h = 0; h < D / 64; ++h)
-            tma_load_2d(ring + slot * L::KV + h * HALF, tm, full, h * 64, t.row0 + c * BN, pol_kv);
-        } else {
-          mbar_arrive(full);
-        }
-        continue;
-      }
-      if (FGA_TMA_GATHER & (1 << kv)) {
-        // TMA tile::gather4: lane l gathers rows 4l..4l+3 of the chunk (both 64-column halves);
-        // rows past the list end repeat the chunk's first key (their scores are masked to -inf,
-        // so their P is 0 and the repeated V row contributes nothing).  The copy engine does
-        // the swizzle, and the SM sub-partition issues 2 instructions per chunk instead of 64
-        // LDGSTS, which would otherwise share the MIO queue with the softmax's MUFU.EX2.
-        const int r0 = c * BN + 4 * lane;
-        const int first = __ldg(t.list + c * BN);
-        int rk[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) rk[e] = t.row0 + (r0 + e < t.count ? __ldg(t.list + r0 + e) : first);
-        mbar_wait(&emptyb[slot], (use & 1) ^ 1);
-        if (lane == 0) mbar_expect_tx(full, BN * D * 2);
-        __syncwarp();
-#pragma unroll
-        for (int h = 0; h < D / 64; ++h)
-          tma_gather4(ring + slot * L::KV + h * HALF + 4 * lane * 128, tmg, full, h * 64, rk[0], rk[1], rk[2], rk[3],
-                      pol_kv);
-        continue;
-      }
-      int keys[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = c * BN + i * 32 + lane;
-        keys[i] = row < t.count ? __ldg(t.list + row) : -1;
-      }
-      mbar_wait(&emptyb[slot], (use & 1) ^ 1);
-      const char* src = gsrc;
-      // opaque to the optimiser, so src + key * 2D stays one IMAD.WIDE.U32 per copy
-      asm volatile("mov.b64 %0, %0;" : "+l"(src));
-      // SW128 destination: row r's 16-byte chunk cc lands at r*128 + ((cc ^ (r & 7)) << 4).  This
-      // lane's rows are mm*RPI + sub (+32i), so (r & 7) cycles with period PER = 8 / RPI in mm and
-      // the address is dstb[mm % PER] + compile-time immediate.
-      constexpr int PER = 8 / RPI;
-      uint32_t dstb[PER];
-#pragma unroll
-      for (int u = 0; u < PER; ++u)
-        dstb[u] = ring_base + slot * L::KV + lane_off + sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
-      if (FGA_NOGATHER) {
-        // timing experiment only: no data movement
-      } else if (c * BN + BN <= t.count) {
-        // full chunk: SHFL + IMAD.WIDE + LDGSTS per 16 bytes
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-#pragma unroll
-          for (int mm = 0; mm < 32 / RPI; ++mm) {
-            const uint32_t key = static_cast<uint32_t>(__shfl_sync(0xffffffffu, keys[i], mm * RPI + sub));
-            const char* g = src + static_cast<size_t>(key) * (D * 2);
-            cp_async16_full(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, g);
-          }
-        }
-      } else {
-        // the tile's last chunk: rows past the list end are zero-filled
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-#pragma unroll
-          for (int mm = 0; mm < 32 / RPI; ++mm) {
-            const int key = __shfl_sync(0xffffffffu, keys[i], mm * RPI + sub);
-            const char* g = src + static_cast<size_t>(static_cast<uint32_t>(max(key, 0))) * (D * 2);
-            cp_async16(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, g, key >= 0 ? 16u : 0u);
-          }
-        }
-      }
-      cp_async_arrive_noinc(full);
-    }
-    base += n;
-  }
-}
-
-// Balanced producers (FGA_PROD_SPLIT): four warps, one per SM sub-partition, each packing
-// one 64-row half of every chunk of one ring (warp 10: K rows 0-63, 11: K rows 64-127,
-// 12: V rows 0-63, 13: V rows 64-127 -> sub-partitions 2, 3, 0, 1).  The LDGSTS traffic,
-// which queues with the softmax's MUFU.EX2 in each sub-partition's MIO unit, is then the
-// same in every TMEM lane quadrant.  A slot completes with both halves' 64 arrivals, so
-// each warp sees every use of every slot of its ring and the empty parity stays exact.
+// Four warps, one per SM sub-partition, each packing one 64-row half of every chunk of one
+// ring (warp 10: K rows 0-63, 11: K rows 64-127, 12: V rows 0-63, 13: V rows 64-127 ->
+// sub-partitions 2, 3, 0, 1): the LDGSTS traffic, which competes with the softmax's
+// MUFU.EX2 for each sub-partition's issue/MIO resources, is the same in every TMEM lane
+// quadrant.  The rings are filled and drained in chunk order; the two issuers free
+// neighbouring chunks out of order, but a slot completes only with both halves' 64
+// arrivals, so each producer sees every use of every slot of its ring and the empty-barrier
+// parity can never be two phases behind.  Per 16 bytes: SHFL of the key, IMAD.WIDE address,
+// LDGSTS into the 128B-swizzled slot; rows past the list end are zero-filled (src-size 0),
+// so no stale or NaN bytes reach the MMA.
 template <int D>
 __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
-                                              const CUtensorMap* tmKg, const CUtensorMap* tmVg, uint8_t* smem,
-                                              const Bars& bar, int kv, int part, int lane) {
+                                              uint8_t* smem, const Bars& bar, int kv, int part, int lane) {
   using L = WsSmem<D>;
   constexpr int LPR = D / 8;     // lanes per 2*D-byte row
   constexpr int RPI = 32 / LPR;  // rows per warp instruction
   constexpr int ROWS = BN / 2;
-  const int nslot = kv ? L::NSV : L::NSK;
+  const int nslot = kv ? NSV : NSK;
   const uint64_t pol_kv = policy_evict_last();
   const int sub = lane / LPR, ch = lane % LPR;
   const uint32_t lane_off = static_cast<uint32_t>((ch >> 3) * HALF);
@@ -327,8 +145,10 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
   uint64_t* fullb = kv ? bar.v_full : bar.k_full;
   uint64_t* emptyb = kv ? bar.v_empty : bar.k_empty;
   const CUtensorMap* tm = kv ? tmV2 : tmK2;
+  // SW128 destination: row r's 16-byte chunk cc lands at r*128 + ((cc ^ (r & 7)) << 4).  This
+  // lane's rows are mm*RPI + sub (+32i), so (r & 7) cycles with period PER = 8 / RPI in mm and
+  // the address is dstb[mm % PER] + compile-time immediate.
   constexpr int PER = 8 / RPI;
-  int knext[ROWS / 32];  // FGA_KEY_PREFETCH: the next chunk's keys
   uint32_t item = 0;
   for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
     const Tile t = decode_tile(p, tile);
@@ -336,7 +156,7 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
     for (int c = 0; c < t.nchunks; ++c, ++item) {
       const uint32_t slot = item % nslot, use = item / nslot;
       uint64_t* full = &fullb[slot];
-      if (p.dense) {
+      if (p.dense) {  // contiguous keys: one TMA box per 64 columns (lane 0 of part 0), 63 arrivals
         mbar_wait(&emptyb[slot], (use & 1) ^ 1);
         if (part == 0 && lane == 0) {
           mbar_expect_tx(full, BN * D * 2);
@@ -352,73 +172,28 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
 #pragma unroll
       for (int i = 0; i < ROWS / 32; ++i) {
         const int row = c * BN + part * ROWS + i * 32 + lane;
-        if (FGA_KEY_PREFETCH && c > 0) keys[i] = knext[i];  // loaded while the previous chunk was copied
-        else keys[i] = row < t.count ? __ldg(t.list + row) : -1;
-      }
-      if (FGA_TMA_ELECT) {
-        // TMA tile::gather4 issued by one elected lane: 16 gather4 x D/64 column blocks for
-        // the 64 rows; rows past the list end repeat the chunk's first key (masked to -inf)
-        const CUtensorMap* tmg = kv ? tmVg : tmKg;
-        const int first = __shfl_sync(0xffffffffu, keys[0], 0);  // row part*64 (< count: chunk non-empty)
-        mbar_wait(&emptyb[slot], (use & 1) ^ 1);
-        if (lane == 0) mbar_expect_tx(full, ROWS * D * 2);
-#pragma unroll 4
-        for (int g = 0; g < ROWS / 4; ++g) {
-          int rk[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int r = 4 * g + e;
-            const int key = __shfl_sync(0xffffffffu, keys[r >> 5], r & 31);
-            rk[e] = t.row0 + (key >= 0 ? key : max(first, 0));
-          }
-          if (elect_one()) {
-#pragma unroll
-            for (int h = 0; h < D / 64; ++h)
-              tma_gather4(ring + slot * L::KV + h * HALF + (part * ROWS + 4 * g) * 128, tmg, full, h * 64, rk[0], rk[1],
-                          rk[2], rk[3], pol_kv);
-          }
-          __syncwarp();
-        }
-        continue;  // lane 0's arrive.expect_tx is this half's arrival
+        keys[i] = row < t.count ? __ldg(t.list + row) : -1;
       }
       mbar_wait(&emptyb[slot], (use & 1) ^ 1);
       const char* src = gsrc;
+      // opaque to the optimiser, so src + key * 2D stays one IMAD.WIDE.U32 per copy
       asm volatile("mov.b64 %0, %0;" : "+l"(src));
       uint32_t dstb[PER];
 #pragma unroll
       for (int u = 0; u < PER; ++u)
         dstb[u] = ring_base + slot * L::KV + lane_off + sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
-      if (c * BN + part * ROWS + ROWS <= t.count) {
-        if (FGA_TMA_MIX > 0) {
-          // the first FGA_TMA_MIX rows of this half by TMA tile::gather4 from one lane (off the MIO
-          // queue the LDGSTS share with the softmax's MUFU), the rest by cp.async below
-          const CUtensorMap* tmg = kv ? tmVg : tmKg;
-          if (lane == 0) mbar_expect_tx(full, FGA_TMA_MIX * D * 2);
-#pragma unroll
-          for (int g = 0; g < FGA_TMA_MIX / 4; ++g) {
-            int rk[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) rk[e] = t.row0 + __shfl_sync(0xffffffffu, keys[0], 4 * g + e);
-            if (elect_one()) {
-#pragma unroll
-              for (int h = 0; h < D / 64; ++h)
-                tma_gather4(ring + slot * L::KV + h * HALF + (part * ROWS + 4 * g) * 128, tmg, full, h * 64, rk[0],
-                            rk[1], rk[2], rk[3], pol_kv);
-            }
-            __syncwarp();
-          }
-        }
+      if (FGA_NOGATHER) {
+        // timing experiment only: no data movement
+      } else if (c * BN + part * ROWS + ROWS <= t.count) {
 #pragma unroll
         for (int i = 0; i < ROWS / 32; ++i) {
 #pragma unroll
           for (int mm = 0; mm < 32 / RPI; ++mm) {
-            if (i * 32 + mm * RPI + RPI <= FGA_TMA_MIX) continue;  // (compile-time) rows gathered by TMA
             const uint32_t key = static_cast<uint32_t>(__shfl_sync(0xffffffffu, keys[i], mm * RPI + sub));
             cp_async16_full(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, src + static_cast<size_t>(key) * (D * 2));
           }
         }
       } else {
-        if (FGA_TMA_MIX > 0 && lane == 0) mbar_arrive(full);  // the arrival the TMA part makes in full chunks
 #pragma unroll
         for (int i = 0; i < ROWS / 32; ++i) {
 #pragma unroll
@@ -427,13 +202,6 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
             const char* g = src + static_cast<size_t>(static_cast<uint32_t>(max(key, 0))) * (D * 2);
             cp_async16(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, g, key >= 0 ? 16u : 0u);
           }
-        }
-      }
-      if (FGA_KEY_PREFETCH) {
-#pragma unroll
-        for (int i = 0; i < ROWS / 32; ++i) {
-          const int row = (c + 1) * BN + part * ROWS + i * 32 + lane;
-          knext[i] = row < t.count ? __ldg(t.list + row) : -1;
         }
       }
       cp_async_arrive_noinc(full);
@@ -470,7 +238,7 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
       const uint32_t c = c0 + j;
       // ---- S_c = Q K_c^T
       {
-        const uint32_t slot = c % L::NSK, use = c / L::NSK;
+        const uint32_t slot = c % NSK, use = c / NSK;
         if (r == 0) FGA_TS(p, it, j, 8);
         mbar_wait(&bar.k_full[slot], use & 1);
         if (r == 0) FGA_TS(p, it, j, 9);
@@ -499,21 +267,21 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
         if (r == 0) FGA_TS(p, it, j, 10);
         mbar_wait(&bar.p_full[r], (c >> 1) & 1);
         if (r == 0) FGA_TS(p, it, j, 11);
-        const uint32_t slot = c % L::NSV, use = c / L::NSV;
+        const uint32_t slot = c % NSV, use = c / NSV;
         mbar_wait(&bar.v_full[slot], use & 1);
         fence_proxy_async_smem();
         tc_fence_after();
         const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
         // Deterministic accumulation: PV_c enters the tensor pipe only after PV_{c-1} (the other
         // issuer's) has been issued, so O sums the chunks in list order on every run.
-        if (FGA_PV_ORDER && c > 0) mbar_wait(bar.pv_issued, (c - 1) & 1);
+        if (c > 0) mbar_wait(bar.pv_issued, (c - 1) & 1);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
             if (!FGA_NOMMA) umma_ts(tO, tS + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, 1u);
           umma_commit(&bar.v_empty[slot]);
           umma_commit(&bar.pv_done[r]);
-          if (FGA_PV_ORDER) mbar_arrive(bar.pv_issued);
+          mbar_arrive(bar.pv_issued);
         }
         __syncwarp();
         if (r == 0) FGA_TS(p, it, j, 12);
@@ -558,13 +326,9 @@ __device__ __forceinline__ void write_q(const AttnParams& p, const void* qptr, c
 }
 
 // P = 2^(s*scale*log2e - m) for this thread's 2 rows x 32 scores: packed FFMA2 for the
-// argument, MUFU ex2 for most pairs and the FMA-pipe polynomial for 1 in POLY_EVERY pairs,
-// packed FADD2 row sums, bf16 pairs in the 16x128b register order.
-// SPLIT_ST: each 64-column half of P is stored to TMEM as soon as it is packed, so the
-// first store's latency overlaps the second half's exps.
-template <bool SPLIT_ST>
+// argument, MUFU ex2, packed FADD2 row sums, bf16 pairs in the 16x128b register order.
 __device__ __forceinline__ void exp_chunk(const uint32_t (&sv)[2][32], float sl2, const float (&m_use)[2],
-                                          uint32_t (&pk)[32], float2 (&sum2)[2][2], uint32_t tS) {
+                                          uint32_t (&pk)[32], float2 (&sum2)[2][2]) {
   const float2 sc2 = make_float2(sl2, sl2);
   const float2 nm[2] = {make_float2(-m_use[0], -m_use[0]), make_float2(-m_use[1], -m_use[1])};
 #pragma unroll
@@ -577,26 +341,10 @@ __device__ __forceinline__ void exp_chunk(const uint32_t (&sv)[2][32], float sl2
       for (int r = 0; r < 2; ++r) {
         const float2 sx = make_float2(__uint_as_float(sv[hh][4 * k + 2 * r]), __uint_as_float(sv[hh][4 * k + 2 * r + 1]));
         const float2 x = __ffma2_rn(sx, sc2, nm[r]);
-        float2 pr;
-        if (FGA_EXP_SKIP > 0 && ((8 * hh + k) * 2 + r) % FGA_EXP_SKIP == 0) {
-          pr = x;  // timing experiment only: no exp for these pairs
-        } else if (FGA_EXP_H2) {
-          pr = ex2_h2(x);
-        } else if (((8 * hh + k) * 2 + r) % POLY_EVERY == POLY_EVERY - 1) {
-          pr = ex2_poly2<FGA_POLY_DEG>(x);
-        } else {
-          pr.x = ex2(x.x);
-          pr.y = ex2(x.y);
-        }
+        const float2 pr = make_float2(ex2(x.x), ex2(x.y));
         sum2[r][k & 1] = __fadd2_rn(sum2[r][k & 1], pr);
         pk[2 * (8 * hh + k) + r] = pack_bf16(pr.x, pr.y);
       }
-    }
-    if constexpr (SPLIT_ST) {
-      uint32_t ph[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) ph[i] = pk[16 * hh + i];
-      tmem_st16x128_x8(tS + 32 * hh, ph);
     }
   }
 }
@@ -620,45 +368,29 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
   int64_t tile = p.tile_begin + blockIdx.x;
   if (tile < p.n_tiles) {
     write_q<D>(p, qptr, decode_tile(p, tile), tmem, q, h, lane);
-    if (!FGA_EPI_WARPS) {
 #pragma unroll
-      for (int i = 0; i < NQ32; ++i) tmem_st32(tOw + i * 32, zero);  // every PV accumulates into O
-    }
+    for (int i = 0; i < NQ32; ++i) tmem_st32(tOw + i * 32, zero);  // every PV accumulates into O
     tmem_st_wait();
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
       mbar_arrive(bar.q_full);
-      if (!FGA_EPI_WARPS) mbar_arrive(bar.o_empty);
+      mbar_arrive(bar.o_empty);
     }
   }
   for (; tile < p.n_tiles; tile += gridDim.x, ++it) {
     const Tile t = decode_tile(p, tile);
-    if (FGA_Q_PREFETCH && tile + gridDim.x < p.n_tiles) {
-      // the next tile's Q rows -> L2 now, so write_q at the end of this tile reads L2, not HBM
-      // (one 128-byte line per thread: 128 rows x 2D bytes)
-      const Tile nt = decode_tile(p, tile + gridDim.x);
-      const int line = tid, lines_per_row = D / 64;
-      if (line < 128 * lines_per_row) {
-        const char* a = static_cast<const char*>(qptr) +
-                        ((static_cast<int64_t>(nt.row0) + nt.q0 + line / lines_per_row) * D) * 2 + (line % lines_per_row) * 128;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-      }
-    }
     float m_use[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};  // l_run: this thread's partial sums
     uint32_t sv[2][32];  // [column half][4k + 2*row + e]: rows r0/r0+8, col 64*half + 8k + 2a + e
-    bool have_s = false;  // sv is already loading S_j (issued at the end of the previous chunk)
     for (int j = 0; j < t.nchunks; ++j) {
       const uint32_t c = chunk + j;
       const uint32_t tS = tmem + TM_S + (c & 1) * 128 + lanes16;
       if (tr) FGA_TS(p, it, j, 0);
-      if (!have_s) {
-        mbar_wait(&bar.s_full[c & 1], (c >> 1) & 1);
-        if (tr) FGA_TS(p, it, j, 1);
-        tc_fence_after();
-        tmem_ld16x256_x8(tS, sv[0]);
-        tmem_ld16x256_x8(tS + 64, sv[1]);
-      }
+      mbar_wait(&bar.s_full[c & 1], (c >> 1) & 1);
+      if (tr) FGA_TS(p, it, j, 1);
+      tc_fence_after();
+      tmem_ld16x256_x8(tS, sv[0]);
+      tmem_ld16x256_x8(tS + 64, sv[1]);
       tmem_ld_wait();
       if (tr) FGA_TS(p, it, j, 2);
       const int nvalid = min(BN, t.count - j * BN);
@@ -689,7 +421,7 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
         sum2[0][0] = sum2[0][1] = sum2[1][0] = sum2[1][1] = make_float2(1.f, 1.f);
         if (j == 0) m_use[0] = m_use[1] = 0.f;
       } else if (!slow) {
-        exp_chunk<FGA_SPLIT_ST>(sv, sl2, m_use, pk, sum2, tS);
+        exp_chunk(sv, sl2, m_use, pk, sum2);
         const float2 u0 = __fadd2_rn(sum2[0][0], sum2[0][1]), u1 = __fadd2_rn(sum2[1][0], sum2[1][1]);
         const bool over = !(u0.x + u0.y <= RESCALE_SUM) || !(u1.x + u1.y <= RESCALE_SUM);
         slow = __any_sync(0xffffffffu, over);
@@ -720,10 +452,10 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
             rescale = true;
           }
         }
-        exp_chunk<FGA_SPLIT_ST>(sv, sl2, m_use, pk, sum2, tS);
+        exp_chunk(sv, sl2, m_use, pk, sum2);
       }
       if (tr) FGA_TS(p, it, j, 3);
-      if (!FGA_SPLIT_ST) tmem_st16x128_x16(tS, pk);
+      tmem_st16x128_x16(tS, pk);
       if (tr) FGA_TS(p, it, j, 4);
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
@@ -747,17 +479,6 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
           }
         }
       }
-      // Load S_{j+1} now if it is ready (it does not depend on P_j), after P_j's store has been
-      // issued, so its TMEM latency overlaps the store wait and the barrier traffic below.
-      have_s = false;
-      if (FGA_PREFETCH_S && j + 1 < t.nchunks &&
-          __all_sync(0xffffffffu, mbar_try_wait(&bar.s_full[(c + 1) & 1], ((c + 1) >> 1) & 1))) {
-        tc_fence_after();
-        const uint32_t tSn = tmem + TM_S + ((c + 1) & 1) * 128 + lanes16;
-        tmem_ld16x256_x8(tSn, sv[0]);
-        tmem_ld16x256_x8(tSn + 64, sv[1]);
-        have_s = true;
-      }
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -780,20 +501,6 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
     for (int r = 0; r < 2; ++r) {
       l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 1);
       l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 2);
-    }
-    if (FGA_EPI_WARPS) {
-      // hand (m, l) to the epilogue warps through buffer it % 2 and go on with the next tile
-      const int buf = it & 1;
-      if (it >= 2) mbar_wait(&bar.stats_empty[buf], ((it >> 1) - 1) & 1);
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-        if (a == 0) {
-          xch[buf * 256 + r0 + 8 * r] = m_use[r];
-          xch[buf * 256 + 128 + r0 + 8 * r] = l_run[r];
-        }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar.stats_full[buf]);
-      continue;
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r)
@@ -830,61 +537,9 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
   }
 }
 
-// ------------------------------------------------------------------ epilogue warps
-// Warp 16 + q (TMEM lane quadrant q, thread = query row): per tile, wait for the softmax's
-// (m, l) and for the tile's last PV, then read O 32 columns at a time, clear it, release it to
-// the next tile's PVs (o_empty) and store O / l (tiled.py:73-77) and the LSE.  The softmax
-// warps meanwhile start on the next tile.
-template <int D, bool OUT_F32>
-__device__ __forceinline__ void epilogue(const AttnParams& p, const Bars& bar, uint32_t tmem, int q, int lane,
-                                         const float* xch) {
-  const int row = q * 32 + lane;
-  const uint32_t tO = tmem + TM_O + (static_cast<uint32_t>(q * 32) << 16);
-  uint32_t zero[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) zero[i] = 0u;
-  int it = 0;
-  int64_t tile = p.tile_begin + blockIdx.x;
-  if (tile < p.n_tiles) {
-#pragma unroll
-    for (int i = 0; i < D / 32; ++i) tmem_st32(tO + i * 32, zero);  // every PV accumulates into O
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar.o_empty);
-  }
-  for (; tile < p.n_tiles; tile += gridDim.x, ++it) {
-    const Tile t = decode_tile(p, tile);
-    const int buf = it & 1;
-    mbar_wait(&bar.stats_full[buf], (it >> 1) & 1);
-    const float mrow = xch[buf * 256 + row], lrow = xch[buf * 256 + 128 + row];
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&bar.stats_empty[buf]);
-    const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
-    mbar_wait(bar.o_full, it & 1);
-    tc_fence_after();
-    const bool valid = row < t.rows;
-    const int64_t out_row = static_cast<int64_t>(t.row0) + t.q0 + row;
-#pragma unroll 1
-    for (int i = 0; i < D / 32; ++i) {  // 32 columns at a time (this warp's register budget)
-      uint32_t o[32];
-      tmem_ld32(tO + i * 32, o);
-      tmem_ld_wait();
-      tmem_st32(tO + i * 32, zero);  // cleared for the next tile
-      if (valid) store_row32<OUT_F32>(p.out, out_row * D + i * 32, o, inv);
-    }
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar.o_empty);  // the next tile's PVs may start
-    if (valid && p.lse != nullptr) p.lse[out_row] = lrow > 0.f ? mrow * 0.69314718055994531f + logf(lrow) : -INFINITY;
-  }
-}
-
 template <int D, bool OUT_F32>
 __global__ void __launch_bounds__(32 * NWARPS, 1)
     fga_attn_ws_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_constant__ CUtensorMap tmV2,
-                       const __grid_constant__ CUtensorMap tmKg, const __grid_constant__ CUtensorMap tmVg,
                        const void* __restrict__ qptr, const AttnParams p) {
   using L = WsSmem<D>;
   extern __shared__ __align__(1024) uint8_t smem_ws[];
@@ -896,21 +551,13 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     if (p.dense) {
       prefetch_tmap(&tmK2);
       prefetch_tmap(&tmV2);
-    } else if (FGA_TMA_GATHER != 0 || FGA_TMA_ELECT || FGA_TMA_MIX > 0) {
-      prefetch_tmap(&tmKg);
-      prefetch_tmap(&tmVg);
     }
-    // a chunk completes with 32 cp.async arrivals (LDGSTS producer, dense path: lane 0's
-    // expect_tx + 31 arrivals) or with lane 0's expect_tx alone (gather4 producer)
-    const uint32_t split_count = (FGA_TMA_ELECT && !p.dense) ? 2u : (FGA_TMA_MIX > 0 && !p.dense) ? 66u : 64u;
-    const uint32_t k_count = FGA_PROD_SPLIT ? split_count : ((FGA_TMA_GATHER & 1) && !p.dense) ? 1u : 32u;
-    const uint32_t v_count = FGA_PROD_SPLIT ? split_count : ((FGA_TMA_GATHER & 2) && !p.dense) ? 1u : 32u;
-    for (int i = 0; i < L::NSK; ++i) {
-      mbar_init(&bar.k_full[i], k_count);  // one producer warp per chunk
+    for (int i = 0; i < NSK; ++i) {
+      mbar_init(&bar.k_full[i], 64);  // both halves' 32 arrivals (dense: lane 0's expect_tx + 63)
       mbar_init(&bar.k_empty[i], 1);
     }
-    for (int i = 0; i < L::NSV; ++i) {
-      mbar_init(&bar.v_full[i], v_count);
+    for (int i = 0; i < NSV; ++i) {
+      mbar_init(&bar.v_full[i], 64);
       mbar_init(&bar.v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -920,12 +567,8 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     }
     mbar_init(bar.q_full, NSOFT);
     mbar_init(bar.o_full, 2);
-    mbar_init(bar.o_empty, FGA_EPI_WARPS ? 4 : NSOFT);
+    mbar_init(bar.o_empty, NSOFT);
     mbar_init(bar.pv_issued, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar.stats_full[i], NSOFT);
-      mbar_init(&bar.stats_empty[i], 4);
-    }
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -951,16 +594,8 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     setmaxnreg_dec<REG_OTHER>();
     if (warp < WARP_PROD0) {
       mma_chain<D>(p, smem, bar, tmem, warp - WARP_MMA0);
-    } else if (FGA_EPI_WARPS && warp >= WARP_EPI0) {
-      epilogue<D, OUT_F32>(p, bar, tmem, warp & 3, lane, reinterpret_cast<const float*>(smem + L::OFF_XCH));
-    } else if (FGA_PROD_SPLIT) {
-      if (warp < WARP_PROD0 + 4)
-        producer_half<D>(p, &tmK2, &tmV2, &tmKg, &tmVg, smem, bar, ((warp - WARP_PROD0) >> 1) ^ FGA_PROD_SWAP,
-                         (warp - WARP_PROD0) & 1, lane);
-    } else if (warp < WARP_PROD0 + NPK) {
-      producer<D>(p, &tmK2, &tmV2, &tmKg, &tmVg, smem, bar, 0, warp - WARP_PROD0, NPK, lane);
-    } else if (warp < WARP_PROD0 + NPK + NPV) {
-      producer<D>(p, &tmK2, &tmV2, &tmKg, &tmVg, smem, bar, 1, warp - WARP_PROD0 - NPK, NPV, lane);
+    } else if (warp < WARP_PROD0 + NPROD) {
+      producer_half<D>(p, &tmK2, &tmV2, smem, bar, (warp - WARP_PROD0) >> 1, (warp - WARP_PROD0) & 1, lane);
     }
   }
   tc_fence_before();
@@ -983,7 +618,7 @@ int launch_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, cudaS
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t span = p.n_tiles - p.tile_begin;
   const int64_t grid = span < sms ? span : sms;
-  kern<<<static_cast<unsigned>(grid), 32 * NWARPS, smem, stream>>>(maps[3], maps[4], maps[1], maps[2], q, p);
+  kern<<<static_cast<unsigned>(grid), 32 * NWARPS, smem, stream>>>(maps[3], maps[4], q, p);
   return check_launch("fga_attn_ws_kernel");
 }
 

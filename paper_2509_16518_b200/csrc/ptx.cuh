@@ -30,28 +30,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-#ifndef FGA_WAIT_HINT_NS
-#define FGA_WAIT_HINT_NS 0  // >0: suspend-time hint of mbarrier.try_wait (ns)
-#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
-  if (FGA_WAIT_HINT_NS > 0) {
-    asm volatile(
-        "{\n.reg .pred P1;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
-        "selp.u32 %0, 1, 0, P1;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity), "n"(FGA_WAIT_HINT_NS)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n.reg .pred P1;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, P1;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
   return ok != 0;
 }
 // Blocking wait with a watchdog: a protocol bug traps (kernel error) after
@@ -355,16 +342,6 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   }
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
-// 2^x for a pair through the half-precision MUFU path (one ex2.approx.f16x2 per pair):
-// x <= 8 here, rounded to f16 (abs. error <= 2^-8 for |x| < 8, i.e. <= 0.27% relative in 2^x).
-__device__ __forceinline__ float2 ex2_h2(float2 x) {
-  uint32_t h;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x.y), "f"(x.x));
-  asm("ex2.approx.f16x2 %0, %0;" : "+r"(h));
-  float2 r;
-  asm("{\n.reg .f16 l, u;\nmov.b32 {l, u}, %2;\ncvt.f32.f16 %0, l;\ncvt.f32.f16 %1, u;\n}" : "=f"(r.x), "=f"(r.y) : "r"(h));
-  return r;
 }
 __device__ __forceinline__ float fmax3f(float a, float b, float c) {
   float m;
