@@ -128,6 +128,7 @@ __device__ __forceinline__ void store_row32(void* out, int64_t off, const uint32
 
 int launch_attn_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, int d, bool out_f32,
                    cudaStream_t stream);
+int launch_attn_dual(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
 int launch_attn_pp(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
 int launch_attn_sync(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
 

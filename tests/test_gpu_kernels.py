@@ -124,13 +124,14 @@ def test_compact_unaligned_rows_without_scores():
 ATTN_CASES = [c for c in GOLDEN_CASES if c != "avgq_topk_ties"]
 
 
-@pytest.fixture(params=["ws", "pp"])
+@pytest.fixture(params=["ws", "pp", "dual"])
 def attn_kernel(request, monkeypatch):
-    """The production kernel (attn_ws.cu) and the ping-pong variant (attn_pp.cu, FGA_ATTN_KERNEL=pp)."""
-    if request.param == "pp":
-        monkeypatch.setenv("FGA_ATTN_KERNEL", "pp")
-    else:
+    """The production kernel (attn_ws.cu) and the variants selected by FGA_ATTN_KERNEL: pp
+    (attn_pp.cu) and dual (attn_dual.cu, groups of 129..256 rows; other shapes fall back to ws)."""
+    if request.param == "ws":
         monkeypatch.delenv("FGA_ATTN_KERNEL", raising=False)
+    else:
+        monkeypatch.setenv("FGA_ATTN_KERNEL", request.param)
     return request.param
 
 
