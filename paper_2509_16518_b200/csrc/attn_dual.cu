@@ -42,8 +42,8 @@ constexpr int REG_OTHER = 72;
 constexpr float RESCALE_THRESHOLD = 8.0f;
 constexpr float RESCALE_SUM = 256.0f;
 constexpr uint32_t TM_O = 0, TM_S = 256;  // O_r at r*128, S_r at 256 + r*128
-#ifndef DU_PASS_AT
-#define DU_PASS_AT 4  // the MUFU turn passes after this many of the row's four 32-score blocks
+#ifndef DU_TURNS
+#define DU_TURNS 1  // the two tiles' softmax warps take turns on each sub-partition's MUFU
 #endif
 
 template <int D>
@@ -53,7 +53,7 @@ struct DuSmem {
   static constexpr int OFF_K = OFF_Q + 2 * KV;
   static constexpr int OFF_V = OFF_K + NSK * KV;
   static constexpr int OFF_BAR = OFF_V + NSV * KV;
-  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 2 + 2;
+  static constexpr int NBAR = 2 * (NSK + NSV) + 4 + 4 + 2 + 2 + 2 + 2;
   static constexpr int OFF_TURN = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;
   static constexpr int BYTES = OFF_TURN + 16;
   static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
@@ -64,8 +64,9 @@ struct Bars {
   uint64_t* k_empty;  // [NSK] count 2: both tiles' S read the chunk
   uint64_t* v_full;   // [NSV] count 64
   uint64_t* v_empty;  // [NSV] count 2: both tiles' PV read the chunk
-  uint64_t* s_full;   // [2] issuer r
-  uint64_t* p_full;   // [2] count 4 (warpgroup r)
+  uint64_t* s_full;   // [2][2] issuer r, 64-key half h
+  uint64_t* p_full;   // [2][2] count 4 (warpgroup r)
+  uint64_t* pv_done;  // [2] issuer r: one completion per PV (two per chunk)
   uint64_t* o_full;   // [2] issuer r: tile r's last PV complete
   uint64_t* o_empty;  // [2] count 4: warpgroup r read and cleared O_r
   uint64_t* q_full;   // Q loader expect_tx (both tiles)
@@ -82,8 +83,9 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   r.v_full = r.k_empty + NSK;
   r.v_empty = r.v_full + NSV;
   r.s_full = r.v_empty + NSV;
-  r.p_full = r.s_full + 2;
-  r.o_full = r.p_full + 2;
+  r.p_full = r.s_full + 4;
+  r.pv_done = r.p_full + 4;
+  r.o_full = r.pv_done + 2;
   r.o_empty = r.o_full + 2;
   r.q_full = r.o_empty + 2;
   r.q_empty = r.q_full + 1;
@@ -177,13 +179,15 @@ __device__ __forceinline__ void q_loader(const AttnParams& p, const CUtensorMap*
 }
 
 // ------------------------------------------------------------------ MMA issuers
-// Issuer r: for every chunk of the group, S_r = Q_r K_c^T, then (after warpgroup r's P)
-// O_r += P_r V_c.  S_r,c+1 overwrites the P that PV_r,c reads; both come from this thread,
-// so tcgen05's in-order execution orders them.
+// Issuer r drives tile r through two chains, one per 64-key half h of each chunk: S_r,c,h =
+// Q_r K_c,h^T (N = 64) into S_r,h, and O_r += P_r,c,h V_c,h (K = 64).  Issue order
+//   S_0,0 S_0,1 | PV_0,0 S_1,0 PV_0,1 S_1,1 | PV_1,0 S_2,0 PV_1,1 S_2,1 | ...
+// puts each S right behind the PV that frees its buffer (tcgen05 executes one thread's ops in
+// order), so while the softmax works on half 1 the tensor core already computes the next half 0.
 template <int D>
 __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, const Bars& bar, uint32_t tmem, int r) {
   using L = DuSmem<D>;
-  constexpr uint32_t IDESC_S = idesc_bf16(BM, BN, false, false);
+  constexpr uint32_t IDESC_S = idesc_bf16(BM, BN / 2, false, false);  // N = 64 keys
   constexpr uint32_t IDESC_O = idesc_bf16(BM, D, false, true);
   const uint64_t dq = sdesc_sw128(smem_u32(smem + L::OFF_Q + r * L::KV), 16, 1024);
   const uint64_t dk0 = sdesc_sw128(smem_u32(smem + L::OFF_K), 16, 1024);
@@ -191,49 +195,63 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
   const uint32_t tO = tmem + TM_O + r * 128, tS = tmem + TM_S + r * 128;
   uint32_t kc = 0;  // CTA-wide chunk counter
   int it = 0;
+  auto issue_s = [&](uint32_t cc, int h, bool last) {  // S_r,cc,h
+    const uint32_t slot = cc % NSK;
+    if (h == 0) {
+      mbar_wait(&bar.k_full[slot], (cc / NSK) & 1);
+      fence_proxy_async_smem();
+      tc_fence_after();
+    }
+    const uint64_t dk = dk0 + ((slot * L::KV + h * 64 * 128) >> 4);
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
+        umma_ss(tS + h * 64, dq + off, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
+      }
+      umma_commit(&bar.s_full[2 * r + h]);
+      if (h == 1) umma_commit(&bar.k_empty[slot]);
+      if (h == 1 && last) umma_commit(bar.q_empty);
+    }
+    __syncwarp();
+  };
+  auto issue_pv = [&](uint32_t cc, int h, bool last) {  // O_r += P_r,cc,h V_cc,h
+    mbar_wait(&bar.p_full[2 * r + h], cc & 1);
+    const uint32_t slot = cc % NSV;
+    if (h == 0) {
+      mbar_wait(&bar.v_full[slot], (cc / NSV) & 1);
+      fence_proxy_async_smem();
+    }
+    tc_fence_after();
+    const uint64_t dv = dv0 + ((slot * L::KV + h * 64 * 128) >> 4);
+    if (elect_one()) {
+#pragma unroll
+      for (int kk = 0; kk < BN / 32; ++kk)
+        umma_ts(tO, tS + h * 64 + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, 1u);
+      umma_commit(&bar.pv_done[r]);
+      if (h == 1) umma_commit(&bar.v_empty[slot]);
+      if (h == 1 && last) umma_commit(&bar.o_full[r]);
+    }
+    __syncwarp();
+  };
   for (int64_t u = blockIdx.x; u < n_groups(p); u += gridDim.x, ++it) {
     const Tile t = group_tile(p, u, r);
+    const int n = t.nchunks;
     mbar_wait(bar.q_full, it & 1);
     tc_fence_after();
-    for (int c = 0; c < t.nchunks; ++c, ++kc) {
-      {  // ---- S_r,c
-        const uint32_t slot = kc % NSK, use = kc / NSK;
-        mbar_wait(&bar.k_full[slot], use & 1);
-        fence_proxy_async_smem();
-        tc_fence_after();
-        const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
-            umma_ss(tS, dq + off, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&bar.s_full[r]);
-          umma_commit(&bar.k_empty[slot]);
-          if (c == t.nchunks - 1) umma_commit(bar.q_empty);
-        }
-        __syncwarp();
-      }
-      {  // ---- O_r += P_r,c V_c
-        if (c == 0) {
-          mbar_wait(&bar.o_empty[r], it & 1);  // O_r cleared by the previous group's epilogue
-          tc_fence_after();
-        }
-        mbar_wait(&bar.p_full[r], kc & 1);
-        const uint32_t slot = kc % NSV, use = kc / NSV;
-        mbar_wait(&bar.v_full[slot], use & 1);
-        fence_proxy_async_smem();
-        tc_fence_after();
-        const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) umma_ts(tO, tS + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, 1u);
-          umma_commit(&bar.v_empty[slot]);
-          if (c == t.nchunks - 1) umma_commit(&bar.o_full[r]);
-        }
-        __syncwarp();
-      }
+    issue_s(kc, 0, n == 1);
+    issue_s(kc, 1, n == 1);
+    mbar_wait(&bar.o_empty[r], it & 1);  // O_r cleared by the previous group's epilogue
+    tc_fence_after();
+    for (int c = 0; c < n; ++c) {
+      const uint32_t cc = kc + c;
+      const bool more = c + 1 < n;
+      issue_pv(cc, 0, !more);
+      if (more) issue_s(cc + 1, 0, c + 2 == n);
+      issue_pv(cc, 1, !more);
+      if (more) issue_s(cc + 1, 1, c + 2 == n);
     }
+    kc += n;
   }
 }
 
@@ -241,50 +259,53 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
 // MUFU turns between the two warps of a sub-partition (attn_pp.cu): tile 0's warp, then
 // tile 1's, for every chunk.  The barriers are tied to the exps through shared memory.
 __device__ __forceinline__ void turn_wait(int q, int r, float& m, uint32_t zero_addr) {
-  asm volatile("{\n.reg .f32 z;\nbar.sync %1, 64;\nld.shared.f32 z, [%2];\nadd.f32 %0, %0, z;\n}\n"
+  if (DU_TURNS) asm volatile("{\n.reg .f32 z;\nbar.sync %1, 64;\nld.shared.f32 z, [%2];\nadd.f32 %0, %0, z;\n}\n"
                : "+f"(m)
                : "r"(2 + 2 * q + r), "r"(zero_addr)
                : "memory");
 }
 __device__ __forceinline__ void turn_pass(int q, int r, float2 a, float2 b, uint32_t junk_addr) {
-  asm volatile("{\n.reg .f32 z;\nadd.f32 z, %0, %1;\nadd.f32 z, z, %2;\nadd.f32 z, z, %3;\n"
+  if (DU_TURNS) asm volatile("{\n.reg .f32 z;\nadd.f32 z, %0, %1;\nadd.f32 z, z, %2;\nadd.f32 z, z, %3;\n"
                "st.shared.f32 [%5], z;\nbar.arrive %4, 64;\n}\n" ::"f"(a.x),
                "f"(a.y), "f"(b.x), "f"(b.y), "r"(2 + 2 * q + (r ^ 1)), "r"(junk_addr)
                : "memory");
 }
 
-__device__ __forceinline__ void load_s(uint32_t tS, uint32_t (&s)[4][32]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i) tmem_ld32(tS + 32 * i, s[i]);
+// 64-key half of a row: 2 x 32 scores
+__device__ __forceinline__ void load_s(uint32_t tS, uint32_t (&s)[2][32]) {
+  tmem_ld32(tS, s[0]);
+  tmem_ld32(tS + 32, s[1]);
   tmem_ld_wait();
 }
 
-__device__ __forceinline__ void mask_tail(uint32_t (&s)[4][32], int nvalid) {
-  if (nvalid < BN) {
+__device__ __forceinline__ void mask_tail(uint32_t (&s)[2][32], int nvalid) {
+  if (nvalid < 64) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int k = 0; k < 32; ++k)
         if (32 * i + k >= nvalid) s[i][k] = __float_as_uint(-INFINITY);
   }
 }
 
-__device__ __forceinline__ float row_max(const uint32_t (&s)[4][32]) {
+__device__ __forceinline__ float row_max(const uint32_t (&s)[2][32]) {
   float m = -INFINITY;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 2; ++i) {
 #pragma unroll
     for (int k = 0; k < 32; k += 2) m = fmax3f(m, __uint_as_float(s[i][k]), __uint_as_float(s[i][k + 1]));
   }
   return m;
 }
 
-__device__ __forceinline__ float exp_row(const uint32_t (&s)[4][32], float sl2, float m, uint32_t (&pk)[64], int q,
-                                         int r, bool pass, uint32_t junk) {
+// P = 2^(s * scale * log2e - m) for the 64 scores: packed FFMA2 arguments, MUFU ex2, packed
+// FADD2 partial sums, key pairs (2i, 2i+1) packed into bf16x2 column i of P.
+__device__ __forceinline__ float exp_half(const uint32_t (&s)[2][32], float sl2, float m, uint32_t (&pk)[32], int q,
+                                          int r, bool pass, uint32_t junk) {
   const float2 sc2 = make_float2(sl2, sl2), nm = make_float2(-m, -m);
   float2 sum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 2; ++i) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[i][2 * k]), __uint_as_float(s[i][2 * k + 1])), sc2, nm);
@@ -292,8 +313,8 @@ __device__ __forceinline__ float exp_row(const uint32_t (&s)[4][32], float sl2, 
       sum[k & 1] = __fadd2_rn(sum[k & 1], pr);
       pk[16 * i + k] = pack_bf16(pr.x, pr.y);
     }
-    if (i == DU_PASS_AT - 1 && pass) turn_pass(q, r, sum[0], sum[1], junk);
   }
+  if (pass) turn_pass(q, r, sum[0], sum[1], junk);
   const float2 u = __fadd2_rn(sum[0], sum[1]);
   return u.x + u.y;
 }
@@ -305,7 +326,7 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const Bars& bar, ui
   const int q = warp & 3, r = warp >> 2;  // lane quadrant, tile of the group
   const int row = q * 32 + lane;
   const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
-  const uint32_t tS = tmem + TM_S + r * 128 + lanes;
+  const uint32_t tSr = tmem + TM_S + r * 128 + lanes;
   const uint32_t tOr = tmem + TM_O + r * 128 + lanes;
   const float sl2 = p.scale_log2;
   uint32_t zero[32];
@@ -326,62 +347,59 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const Bars& bar, ui
     const Tile t = group_tile(p, u, r);
     float m = -INFINITY, l = 0.f;
     for (int c = 0; c < t.nchunks; ++c, ++kc) {
-      mbar_wait(&bar.s_full[r], kc & 1);
-      tc_fence_after();
-      uint32_t s[4][32];
-      load_s(tS, s);
-      const int nvalid = min(BN, t.count - c * BN);
-      mask_tail(s, nvalid);
-      uint32_t pk[64];
-      float alpha = 1.f, sum;
-      bool rescale = false;
-      if (c == 0) {
-        m = row_max(s) * sl2;
-        turn_wait(q, r, m, zaddr);
-        sum = exp_row(s, sl2, m, pk, q, r, true, junk);
-      } else {
-        turn_wait(q, r, m, zaddr);
-        sum = exp_row(s, sl2, m, pk, q, r, true, junk);
-        if (__any_sync(0xffffffffu, !(sum <= RESCALE_SUM))) {
-          // S is still intact in TMEM (P not yet stored): reload, move the running max, recompute
-          load_s(tS, s);
-          mask_tail(s, nvalid);
-          const float rmax = row_max(s) * sl2;
-          if (rmax - m > RESCALE_THRESHOLD) {
-            alpha = ex2(m - rmax);
-            m = rmax;
-            rescale = true;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t tS = tSr + h * 64;
+        mbar_wait(&bar.s_full[2 * r + h], kc & 1);
+        tc_fence_after();
+        uint32_t s[2][32];
+        load_s(tS, s);
+        const int nvalid = min(64, t.count - c * BN - h * 64);  // may be <= 0 in a short last chunk
+        mask_tail(s, nvalid);
+        uint32_t pk[32];
+        float alpha = 1.f, sum;
+        bool rescale = false;
+        if (c == 0 && h == 0) {
+          m = row_max(s) * sl2;
+          turn_wait(q, r, m, zaddr);
+          sum = exp_half(s, sl2, m, pk, q, r, true, junk);
+        } else {
+          turn_wait(q, r, m, zaddr);
+          sum = exp_half(s, sl2, m, pk, q, r, true, junk);
+          if (__any_sync(0xffffffffu, !(sum <= RESCALE_SUM))) {
+            load_s(tS, s);  // S is intact (P not yet stored)
+            mask_tail(s, nvalid);
+            const float rmax = row_max(s) * sl2;
+            if (rmax - m > RESCALE_THRESHOLD) {
+              alpha = ex2(m - rmax);
+              m = rmax;
+              rescale = true;
+            }
+            sum = exp_half(s, sl2, m, pk, q, r, false, junk);
           }
-          sum = exp_row(s, sl2, m, pk, q, r, false, junk);
         }
-      }
-      if (__any_sync(0xffffffffu, rescale)) {
-        // S_r,c complete => this tile's previous PV (same issuer, issued before it) is complete
+        if (__any_sync(0xffffffffu, rescale)) {
+          // every PV issued into O_r so far (2*kc + h of them) must have landed before O_r scales
+          const uint32_t done = 2 * kc + h;
+          mbar_wait(&bar.pv_done[r], (done - 1) & 1);
+          tc_fence_after();
 #pragma unroll
-        for (int i = 0; i < D / 32; ++i) {
-          uint32_t o[32];
-          tmem_ld32(tOr + 32 * i, o);
-          tmem_ld_wait();
+          for (int i = 0; i < D / 32; ++i) {
+            uint32_t o[32];
+            tmem_ld32(tOr + 32 * i, o);
+            tmem_ld_wait();
 #pragma unroll
-          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
-          tmem_st32(tOr + 32 * i, o);
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+            tmem_st32(tOr + 32 * i, o);
+          }
         }
+        l = l * alpha + sum;
+        tmem_st32(tS, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar.p_full[2 * r + h]);
       }
-      l = l * alpha + sum;
-      {
-        uint32_t a[32], b[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          a[k] = pk[k];
-          b[k] = pk[32 + k];
-        }
-        tmem_st32(tS, a);
-        tmem_st32(tS + 32, b);
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar.p_full[r]);
     }
     // ---- epilogue of tile r (tiled.py:73-77)
     mbar_wait(&bar.o_full[r], it & 1);
@@ -403,7 +421,7 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const Bars& bar, ui
     if (lane == 0) mbar_arrive(&bar.o_empty[r]);
     if (valid && p.lse != nullptr) p.lse[out_row] = l > 0.f ? m * 0.69314718055994531f + logf(l) : -INFINITY;
   }
-  if (kc > 0 && r == 0) {  // the turn tile 1's warp passed after the last chunk
+  if (kc > 0 && r == 0) {  // the turn tile 1's warp passed after the last half-chunk
     float dummy = 0.f;
     turn_wait(q, r, dummy, zaddr);
   }
@@ -428,9 +446,12 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
       mbar_init(&bar.v_full[i], 64);
       mbar_init(&bar.v_empty[i], 2);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&bar.s_full[i], 1);
       mbar_init(&bar.p_full[i], NSOFT / 2);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar.pv_done[i], 1);
       mbar_init(&bar.o_full[i], 1);
       mbar_init(&bar.o_empty[i], NSOFT / 2);
     }
