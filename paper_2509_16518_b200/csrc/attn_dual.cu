@@ -53,17 +53,17 @@ struct DuSmem {
   static constexpr int OFF_K = OFF_Q + 2 * KV;
   static constexpr int OFF_V = OFF_K + NSK * KV;
   static constexpr int OFF_BAR = OFF_V + NSV * KV;
-  static constexpr int NBAR = 2 * (NSK + NSV) + 4 + 4 + 2 + 2 + 2 + 2;
+  static constexpr int NBAR = 3 * (NSK + NSV) + 4 + 4 + 2 + 2 + 2 + 2;
   static constexpr int OFF_TURN = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;
-  static constexpr int BYTES = OFF_TURN + 16;
+  static constexpr int BYTES = OFF_TURN + 4 + 256 * 4;  // the 0.0f word + one scratch word per softmax thread
   static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
 struct Bars {
   uint64_t* k_full;   // [NSK] count 64 (two producer halves)
-  uint64_t* k_empty;  // [NSK] count 2: both tiles' S read the chunk
+  uint64_t* k_empty;  // [2][NSK] issuer r's S read the chunk (the producers wait for both)
   uint64_t* v_full;   // [NSV] count 64
-  uint64_t* v_empty;  // [NSV] count 2: both tiles' PV read the chunk
+  uint64_t* v_empty;  // [2][NSV] issuer r's PV read the chunk
   uint64_t* s_full;   // [2][2] issuer r, 64-key half h
   uint64_t* p_full;   // [2][2] count 4 (warpgroup r)
   uint64_t* pv_done;  // [2] issuer r: one completion per PV (two per chunk)
@@ -80,9 +80,9 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   Bars r;
   r.k_full = b;
   r.k_empty = r.k_full + NSK;
-  r.v_full = r.k_empty + NSK;
+  r.v_full = r.k_empty + 2 * NSK;
   r.v_empty = r.v_full + NSV;
-  r.s_full = r.v_empty + NSV;
+  r.s_full = r.v_empty + 2 * NSV;
   r.p_full = r.s_full + 4;
   r.pv_done = r.p_full + 4;
   r.o_full = r.pv_done + 2;
@@ -124,7 +124,12 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem
         const int row = c * BN + part * ROWS + i * 32 + lane;
         keys[i] = row < t.count ? __ldg(t.list + row) : -1;
       }
-      mbar_wait(&emptyb[slot], (use & 1) ^ 1);
+      mbar_wait(&emptyb[slot], (use & 1) ^ 1);          // tile 0's reads of the slot done
+      mbar_wait(&emptyb[nslot + slot], (use & 1) ^ 1);  // and tile 1's
+      // this thread's copies into the slot's previous use completed before the slot filled (the
+      // empty waits imply it); the wait states it for tools that track cp.async per thread
+      // (compute-sanitizer racecheck), and is a no-op here
+      if (use > 0) asm volatile("cp.async.wait_group %0;" ::"n"(NSK > NSV ? NSV - 1 : NSK - 1) : "memory");
       const char* src = gsrc;
       asm volatile("mov.b64 %0, %0;" : "+l"(src));
       uint32_t dstb[PER];
@@ -152,6 +157,7 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem
         }
       }
       cp_async_arrive_noinc(&fullb[slot]);
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
   }
 }
@@ -210,7 +216,7 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
         umma_ss(tS + h * 64, dq + off, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
       }
       umma_commit(&bar.s_full[2 * r + h]);
-      if (h == 1) umma_commit(&bar.k_empty[slot]);
+      if (h == 1) umma_commit(&bar.k_empty[r * NSK + slot]);
       if (h == 1 && last) umma_commit(bar.q_empty);
     }
     __syncwarp();
@@ -229,7 +235,7 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
       for (int kk = 0; kk < BN / 32; ++kk)
         umma_ts(tO, tS + h * 64 + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, 1u);
       umma_commit(&bar.pv_done[r]);
-      if (h == 1) umma_commit(&bar.v_empty[slot]);
+      if (h == 1) umma_commit(&bar.v_empty[r * NSV + slot]);
       if (h == 1 && last) umma_commit(&bar.o_full[r]);
     }
     __syncwarp();
@@ -321,7 +327,7 @@ __device__ __forceinline__ float exp_half(const uint32_t (&s)[2][32], float sl2,
 
 template <int D, bool OUT_F32>
 __device__ __forceinline__ void softmax(const AttnParams& p, const Bars& bar, uint32_t tmem, int tid, uint32_t zaddr) {
-  const uint32_t junk = zaddr + 4;
+  const uint32_t junk = zaddr + 4 + 4 * tid;  // per-thread scratch word: no write-write sharing
   const int warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, r = warp >> 2;  // lane quadrant, tile of the group
   const int row = q * 32 + lane;
@@ -438,14 +444,10 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     prefetch_tmap(&tmQ);
-    for (int i = 0; i < NSK; ++i) {
-      mbar_init(&bar.k_full[i], 64);
-      mbar_init(&bar.k_empty[i], 2);
-    }
-    for (int i = 0; i < NSV; ++i) {
-      mbar_init(&bar.v_full[i], 64);
-      mbar_init(&bar.v_empty[i], 2);
-    }
+    for (int i = 0; i < NSK; ++i) mbar_init(&bar.k_full[i], 64);
+    for (int i = 0; i < 2 * NSK; ++i) mbar_init(&bar.k_empty[i], 1);
+    for (int i = 0; i < NSV; ++i) mbar_init(&bar.v_full[i], 64);
+    for (int i = 0; i < 2 * NSV; ++i) mbar_init(&bar.v_empty[i], 1);
     for (int i = 0; i < 4; ++i) {
       mbar_init(&bar.s_full[i], 1);
       mbar_init(&bar.p_full[i], NSOFT / 2);

@@ -82,7 +82,7 @@ struct PpSmem {
   static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 4;
   static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row per group
   static constexpr int OFF_TURN = OFF_XCH + 4 * 128 * 4;  // a 0.0f word and a scratch word (turn_wait/pass)
-  static constexpr int BYTES = OFF_TURN + 16;
+  static constexpr int BYTES = OFF_TURN + 4 + 8 * 4;  // the 0.0f word + one scratch word per softmax warp (SMEM is full)
   static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
@@ -393,7 +393,7 @@ __device__ __forceinline__ float exp_row(const uint32_t (&s)[4][32], float sl2, 
 template <int D, bool OUT_F32>
 __device__ __forceinline__ void softmax(const AttnParams& p, const Bars& bar, uint32_t tmem, int tid, float* xch,
                                         uint32_t zaddr) {
-  const uint32_t junk = zaddr + 4;
+  const uint32_t junk = zaddr + 4 + 4 * (tid >> 5);  // per-warp scratch word (its lanes write the same word: benign)
   const int warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, r = warp >> 2;  // lane quadrant, softmax group (= chunk parity)
   const int row = q * 32 + lane;

@@ -353,9 +353,9 @@ int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx,
   }
   if (which != nullptr && std::strcmp(which, "sync") == 0) return launch_attn_sync(maps, p, static_cast<int>(D), f32, stream);
   if (which != nullptr && std::strcmp(which, "pp") == 0) return launch_attn_pp(maps, p, static_cast<int>(D), f32, stream);
-  // FGA_ATTN_KERNEL=dual: groups of 129..256 rows with both tiles of a group sharing each gathered
-  // chunk (attn_dual.cu; correct, but not faster than attn_ws.cu yet -- DESIGN.md section 4)
-  if (which != nullptr && std::strcmp(which, "dual") == 0) {
+  // groups of 129..256 rows: both tiles of a group share each gathered chunk (attn_dual.cu, 1-7%
+  // faster than attn_ws.cu there); FGA_ATTN_KERNEL=ws forces attn_ws.cu
+  if (which == nullptr || std::strcmp(which, "ws") != 0) {
     const int rc = launch_attn_dual(maps, p, static_cast<int>(D), f32, stream);
     if (rc != FGA_EUNSUPPORTED) return rc;
   }

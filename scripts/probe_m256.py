@@ -1,5 +1,5 @@
-"""Sparse attention with 256-row query groups: the shared-gather dual-tile kernel vs the per-tile
-kernel (default), c2 shape; FGA_ATTN_KERNEL=dual selects the former (development aid)."""
+"""Sparse attention with 129..256-row query groups: the shared-gather dual-tile kernel (default for
+those shapes) vs the per-tile kernel (FGA_ATTN_KERNEL=ws), c2 shape (development aid)."""
 import os
 import sys
 

@@ -124,11 +124,11 @@ def test_compact_unaligned_rows_without_scores():
 ATTN_CASES = [c for c in GOLDEN_CASES if c != "avgq_topk_ties"]
 
 
-@pytest.fixture(params=["ws", "pp", "dual"])
+@pytest.fixture(params=["default", "ws", "pp"])
 def attn_kernel(request, monkeypatch):
-    """The production kernel (attn_ws.cu) and the variants selected by FGA_ATTN_KERNEL: pp
-    (attn_pp.cu) and dual (attn_dual.cu, groups of 129..256 rows; other shapes fall back to ws)."""
-    if request.param == "ws":
+    """The default dispatch (attn_ws.cu; attn_dual.cu for groups of 129..256 rows) and the kernels
+    FGA_ATTN_KERNEL selects: ws (attn_ws.cu for every shape) and pp (attn_pp.cu)."""
+    if request.param == "default":
         monkeypatch.delenv("FGA_ATTN_KERNEL", raising=False)
     else:
         monkeypatch.setenv("FGA_ATTN_KERNEL", request.param)
