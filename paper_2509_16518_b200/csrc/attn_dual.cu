@@ -7,15 +7,16 @@
 // same rows, so gathering them once per group halves the L2->SMEM bytes per FLOP, which is
 // what bounds the single-tile kernel.
 //
-// Work unit = one group.  Per chunk c of its list:
-//   S_r,c = Q_r K_c^T     tcgen05 SS-MMA, r = tile 0 / 1 (Q tiles in SMEM, TMA)
-//   P_r,c = 2^(S * scale * log2e - m_r)   softmax warpgroup r (thread = query row)
-//   O_r  += P_r,c V_c     TS-MMA (P from TMEM, V from SMEM)
-// TMEM (512 columns): O_0 | O_1 | S_0 | S_1 (the attn_pp.cu layout); each tile keeps its own
-// running max and accumulator, so the epilogues need no exchange.  Warpgroup r's next S can
-// only be issued after its PV (one S buffer per tile), so the two tiles' chains interleave on
-// the tensor core, and the warpgroups take turns on each sub-partition's MUFU (attn_pp.cu's
-// named-barrier turns) so one exponentiates while the tensor core serves the other.
+// Work unit = one group.  Per chunk c of its list and 64-key half h of the chunk:
+//   S_r,c,h = Q_r K_c,h^T   tcgen05 SS-MMA (N = 64), r = tile 0 / 1 (Q tiles in SMEM, TMA)
+//   P_r,c,h = 2^(S * scale * log2e - m_r)   softmax warpgroup r (thread = query row)
+//   O_r    += P_r,c,h V_c,h  TS-MMA (K = 64; P from TMEM, V from SMEM)
+// TMEM (512 columns): O_0 | O_1 | S_0,0 S_0,1 | S_1,0 S_1,1 (64 columns each); each tile keeps its
+// own running max and accumulator, so the epilogues need no exchange.  The two halves are two
+// chains per tile (S_c+1,h reuses the buffer PV_c,h reads, issued right behind it), and the two
+// warpgroups take turns on each sub-partition's MUFU (attn_pp.cu's named-barrier turns) so one
+// exponentiates while the tensor core serves the other.  Default for 129..256-row groups
+// (1-7% faster than attn_ws.cu there).
 //
 // Warps (16): 0-3 softmax tile 0, 4-7 softmax tile 1, 8/9 MMA issuer of tile 0/1, 10-13
 // gather producers (64-row halves of every K / V chunk, one per sub-partition), 14 Q loader.
