@@ -249,6 +249,19 @@ def test_batched_heads(b, h, n, d, attn_kernel):
     assert np.abs(o.cpu().numpy() - ref).max() <= ATOL
 
 
+@pytest.mark.parametrize("n,m", [(1, 1), (7, 7), (7, 1), (50, 50), (130, 3), (300, 300)])
+def test_tiny_and_degenerate_shapes(n, m, attn_kernel):
+    # single-row groups, one short tile, groups longer than a tile but shorter than two
+    b, h, d = 1, 2, 64
+    rng = np.random.default_rng(n * 31 + m)
+    q, k, v = (oracle.bf16_round(rng.standard_normal((b, h, n, d)).astype(np.float32)) for _ in range(3))
+    lists = oracle.random_lists(b, h, n, m, 0.5, seed=n + m)
+    ref = oracle.masked_attention(q, k, v, lists, m)
+    idx, cnt = padded_dev(lists, b, h, n, m)
+    o, _ = run_sparse(to_bf16_dev(q), to_bf16_dev(k), to_bf16_dev(v), idx, cnt, b, h, n, d, m)
+    assert np.abs(o.cpu().numpy() - ref).max() <= ATOL
+
+
 @pytest.mark.parametrize("m", [16, 64, 200, 256])
 def test_group_sizes(m, attn_kernel):
     b, h, n, d = 1, 2, 600, 64
