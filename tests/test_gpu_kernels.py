@@ -124,10 +124,11 @@ def test_compact_unaligned_rows_without_scores():
 ATTN_CASES = [c for c in GOLDEN_CASES if c != "avgq_topk_ties"]
 
 
-@pytest.fixture(params=["default", "ws", "pp"])
+@pytest.fixture(params=["default", "ws", "pp", "sync"])
 def attn_kernel(request, monkeypatch):
     """The default dispatch (attn_ws.cu; attn_dual.cu for groups of 129..256 rows) and the kernels
-    FGA_ATTN_KERNEL selects: ws (attn_ws.cu for every shape) and pp (attn_pp.cu)."""
+    FGA_ATTN_KERNEL selects: ws (attn_ws.cu for every shape), pp (attn_pp.cu) and sync (the
+    round-1 synchronous 4-warp kernel in attn_sm100.cu, kept as the simple baseline)."""
     if request.param == "default":
         monkeypatch.delenv("FGA_ATTN_KERNEL", raising=False)
     else:
