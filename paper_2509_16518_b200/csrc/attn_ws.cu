@@ -54,7 +54,13 @@ constexpr int NPROD = 4;      // gather producers 10-13
 constexpr int NWARPS = 16;
 constexpr int REG_SOFTMAX = 184;
 constexpr int REG_OTHER = 72;  // producers and issuers: measured 13% slower at 64
-constexpr int NSK = 3, NSV = 3;  // K / V ring slots
+#ifndef FGA_NSK
+#define FGA_NSK 3
+#endif
+#ifndef FGA_NSV
+#define FGA_NSV 3
+#endif
+constexpr int NSK = FGA_NSK, NSV = FGA_NSV;  // K / V ring slots
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units (factor 256)
 constexpr float RESCALE_SUM = 256.0f;      // 2^RESCALE_THRESHOLD
 constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
