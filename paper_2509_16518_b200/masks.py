@@ -23,9 +23,9 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._device import as_device, as_device_bf16, is_torch, ptr, require_device, stream_ptr, torch
+from ._device import as_device, as_device_bf16, is_torch, ptr, stream_ptr, torch
 from .core import AttnConfig, ShapeError
-from .sparse import DeviceIndexMask, SparseIndexMask, compact_keep
+from .sparse import compact_keep
 
 __all__ = [
     "STRATEGIES", "MaskBuilderConfig", "CachedMaskState", "refresh_policy", "build_mask_cached",
