@@ -19,6 +19,11 @@ namespace fga {
 namespace {
 
 constexpr int T = 256;
+#ifndef FGA_COMPACT_T
+#define FGA_COMPACT_T 256
+#endif
+constexpr int TC = FGA_COMPACT_T;  // keep-byte kernel: threads per row (one 16-byte block each per round)
+constexpr int WC = TC / 32;
 constexpr int W = T / 32;
 
 __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t x) {
@@ -28,15 +33,15 @@ __device__ __forceinline__ uint32_t nonzero_bytes(uint32_t x) {
   return m;
 }
 
-__global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restrict__ keep,
+__global__ void __launch_bounds__(TC) fga_compact_kernel(const uint8_t* __restrict__ keep,
                                                         const float* __restrict__ scores, int64_t n,
                                                         int32_t* __restrict__ idx, int64_t stride,
                                                         int32_t* __restrict__ counts, int fill) {
-  __shared__ int s_warp[W];
+  __shared__ int s_warp[WC];
   __shared__ int s_total;
-  __shared__ float s_bv[W];
-  __shared__ int s_bi[W];
-  __shared__ int s_stage[T * 16];  // one round's positions, written out coalesced
+  __shared__ float s_bv[WC];
+  __shared__ int s_bi[WC];
+  __shared__ int s_stage[TC * 16];  // one round's positions, written out coalesced
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint8_t* kr = keep + row * n;
@@ -54,10 +59,10 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
   };
   uint4 wn = load(tid);
   int running = 0;
-  for (int64_t b0 = 0; b0 < nblk; b0 += T) {
+  for (int64_t b0 = 0; b0 < nblk; b0 += TC) {
     const int64_t blk = b0 + tid;
     const uint4 w = wn;
-    wn = load(blk + T);
+    wn = load(blk + TC);
     uint32_t bits = 0;
     if (blk < nblk) {
       const int64_t lo = blk * 16;
@@ -81,15 +86,15 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-      const int v = lane < W ? s_warp[lane] : 0;
+      const int v = lane < WC ? s_warp[lane] : 0;
       int sc = v;
 #pragma unroll
-      for (int o = 1; o < W; o <<= 1) {
+      for (int o = 1; o < WC; o <<= 1) {
         const int t = __shfl_up_sync(0xffffffffu, sc, o);
         if (lane >= o) sc += t;
       }
-      if (lane < W) s_warp[lane] = sc - v;  // exclusive warp prefix
-      if (lane == W - 1) s_total = sc;
+      if (lane < WC) s_warp[lane] = sc - v;  // exclusive warp prefix
+      if (lane == WC - 1) s_total = sc;
     }
     __syncthreads();
     int off = s_warp[warp] + incl - cnt;
@@ -100,7 +105,7 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
     }
     __syncthreads();
     const int total = s_total;
-    for (int i = tid; i < total; i += T) out[running + i] = s_stage[i];
+    for (int i = tid; i < total; i += TC) out[running + i] = s_stage[i];
     running += total;
     __syncthreads();
   }
@@ -110,7 +115,7 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
     const float* sr = scores + row * n;
     float bv = -INFINITY;
     int bi = 0x7fffffff;
-    for (int64_t i = tid; i < n; i += T) {
+    for (int64_t i = tid; i < n; i += TC) {
       const float x = sr[i];
       if (x > bv || (x == bv && i < bi)) { bv = x; bi = static_cast<int>(i); }
     }
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
     if (lane == 0) { s_bv[warp] = bv; s_bi[warp] = bi; }
     __syncthreads();
     if (tid == 0) {
-      for (int w = 1; w < W; ++w)
+      for (int w = 1; w < WC; ++w)
         if (s_bv[w] > bv || (s_bv[w] == bv && s_bi[w] < bi)) { bv = s_bv[w]; bi = s_bi[w]; }
       out[0] = bi == 0x7fffffff ? 0 : bi;  // all -inf / NaN rows: index 0 like np.argmax
     }
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(T) fga_compact_kernel(const uint8_t* __restric
   }
   if (tid == 0) counts[row] = running;
   if (fill)
-    for (int64_t i = running + tid; i < n; i += T) out[i] = -1;
+    for (int64_t i = running + tid; i < n; i += TC) out[i] = -1;
 }
 
 // ---------------------------------------------------------------- bit-packed masks
@@ -247,7 +252,7 @@ int launch_compact(const uint8_t* keep, const float* scores, int64_t rows, int64
   if (n >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact: n must be < 2^31");
   if (rows == 0) return FGA_OK;
   if (rows >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact: too many rows");
-  fga_compact_kernel<<<static_cast<unsigned>(rows), T, 0, stream>>>(keep, scores, n, idx, idx_stride, counts, fill);
+  fga_compact_kernel<<<static_cast<unsigned>(rows), TC, 0, stream>>>(keep, scores, n, idx, idx_stride, counts, fill);
   return check_launch("fga_compact_kernel");
 }
 
