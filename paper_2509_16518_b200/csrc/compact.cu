@@ -7,115 +7,196 @@
 // Two input formats: uint8 keep bytes (fga_compact) and bit-packed keep words
 // (fga_compact_bits, 8x fewer bytes to read or to ship from the host).
 //
-// One CTA per (b,h,g) row.  Each thread reads one aligned 16-byte block of
-// keep bytes per round, turns it into a 16-bit occupancy mask, and a
-// warp-shuffle + shared-memory block scan of the popcounts gives every
-// thread its offset in a shared-memory stage, so positions come out in
-// ascending order without any sort and leave the CTA as coalesced stores.
+// One 256-thread CTA per (b,h,g) row, walked in rounds of 8 warps x SPW steps
+// of 1024 keys: warp w owns the contiguous steps [SPW*w, SPW*w + SPW) of the
+// round, so every lane issues all SPW steps' loads before it needs any of
+// them (keep bytes: lane l loads the 16-byte blocks at 16l and 512 + 16l of a
+// step, two coalesced LDG.128; keep bits: word l of the step).  Per step a lane
+// turns its bytes into two 16-bit occupancy masks with byte-SIMD arithmetic
+// and ONE warp scan of the packed counts (low half: first 512 keys of the
+// step, high half: last 512) gives its two offsets; the SPW scans are
+// independent, so they overlap.  One __syncthreads per round exchanges the
+// warp totals.  Each lane then emits its kept positions into its warp's
+// shared-memory stage with an unrolled predicated loop (no divergence) and
+// after a __syncwarp the warp writes the step's positions out coalesced; the
+// stage is double-buffered per warp so that is the only synchronisation.
+// Positions come out ascending, bit-exact with np.nonzero, with no sort.
 // HBM-bound: read n bytes (n/8 for bits), write 4*count (+4*(n-count)).
+// (Round-1 history: a block scan per 16 keys per thread was issue-bound at 80%
+// issue-slot utilisation, 3.2 TB/s — ~270 instructions of per-round overhead
+// per warp; one warp per row removed the barriers but left one serial step
+// chain per warp with ~21 warps per SM: 2.5 TB/s.)
 #include "internal.h"
 
 namespace fga {
 namespace {
 
-constexpr int T = 256;
-#ifndef FGA_COMPACT_T
-#define FGA_COMPACT_T 256
-#endif
-constexpr int TC = FGA_COMPACT_T;  // keep-byte kernel: threads per row (one 16-byte block each per round)
-constexpr int WC = TC / 32;
-constexpr int W = T / 32;
+constexpr int STEP = 1024;  // keys per warp step
+constexpr int WARPS = 8;
+constexpr int SPW = 4;      // steps per warp per round: a round is 32768 keys (c2's whole row)
 
-__device__ __forceinline__ uint32_t nonzero_bytes(uint32_t x) {
-  uint32_t m = 0;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) m |= ((x >> (8 * e)) & 0xFFu) ? (1u << e) : 0u;
-  return m;
+// bit k of the result = (byte k of x != 0), k = 0..3
+__device__ __forceinline__ uint32_t nz4(uint32_t x) {
+  const uint32_t h = (((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;  // bit 7 of each nonzero byte
+  return ((h >> 7) * 0x01020408u) >> 24;                                       // gather the 4 bits
+}
+__device__ __forceinline__ uint32_t nz16(const uint4& w) {
+  return nz4(w.x) | (nz4(w.y) << 4) | (nz4(w.z) << 8) | (nz4(w.w) << 12);
 }
 
-__global__ void __launch_bounds__(TC) fga_compact_kernel(const uint8_t* __restrict__ keep,
-                                                        const float* __restrict__ scores, int64_t n,
-                                                        int32_t* __restrict__ idx, int64_t stride,
-                                                        int32_t* __restrict__ counts, int fill) {
-  __shared__ int s_warp[WC];
-  __shared__ int s_total;
-  __shared__ float s_bv[WC];
-  __shared__ int s_bi[WC];
-  __shared__ int s_stage[TC * 16];  // one round's positions, written out coalesced
+// emit base-relative positions rel0 + e for the set bits e of a 16-bit mask
+__device__ __forceinline__ void emit16(uint16_t* st, int off, uint32_t m, int rel0) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    if (m & (1u << e)) st[off++] = static_cast<uint16_t>(rel0 + e);
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+struct Blk2 {
+  uint4 a, b;
+};
+
+// keep bytes: one step's data for this lane
+struct ByteSrc {
+  const uint8_t* abase;  // 16-byte aligned start of the row's bytes
+  int head, span;        // the row is abase[head, span)  (n < 2^31)
+  int lane;
+  __device__ __forceinline__ uint4 ld(int lo) const {
+    return (lo >= head && lo + 16 <= span) ? __ldg(reinterpret_cast<const uint4*>(abase + lo))
+                                           : make_uint4(0u, 0u, 0u, 0u);
+  }
+  __device__ __forceinline__ Blk2 load(int64_t s) const {
+    const int lo = static_cast<int>(s) * STEP + lane * 16;
+    return Blk2{ld(lo), ld(lo + STEP / 2)};
+  }
+  __device__ __noinline__ uint32_t mask_edge(int lo) const {  // the row's ragged ends
+    uint32_t m = 0;
+    for (int e = 0; e < 16; ++e) {
+      const int pos = lo + e;
+      if (pos >= head && pos < span && abase[pos] != 0) m |= 1u << e;
+    }
+    return m;
+  }
+  __device__ __forceinline__ uint32_t mask16(const uint4& w, int lo) const {
+    if (lo >= head && lo + 16 <= span) return nz16(w);
+    return (lo < span && lo + 16 > head) ? mask_edge(lo) : 0u;
+  }
+  // masks of the step's two 16-key blocks (half 0: keys 16l.., half 1: 512 + 16l..)
+  __device__ __forceinline__ void masks(const Blk2& d, int64_t s, uint32_t& m0, uint32_t& m1) const {
+    const int lo = static_cast<int>(s) * STEP + lane * 16;
+    m0 = mask16(d.a, lo);
+    m1 = mask16(d.b, lo + STEP / 2);
+  }
+  static constexpr bool kHalfMajor = true;  // all lanes' half 0, then all lanes' half 1
+  __device__ __forceinline__ int key_base(int64_t s) const { return static_cast<int>(s) * STEP - head; }
+};
+
+// keep bits: word l of the step
+struct BitSrc {
+  const uint32_t* br;
+  int64_t words, n;
+  int lane;
+  __device__ __forceinline__ uint32_t load(int64_t s) const {
+    const int64_t w = s * 32 + lane;
+    return w < words ? __ldg(br + w) : 0u;
+  }
+  __device__ __forceinline__ void masks(uint32_t v, int64_t s, uint32_t& m0, uint32_t& m1) const {
+    const int64_t k0 = (s * 32 + lane) * 32;
+    if (k0 + 32 > n) v &= (k0 >= n) ? 0u : ((1u << (n - k0)) - 1u);  // keys past n are not keys
+    m0 = v & 0xFFFFu;
+    m1 = v >> 16;
+  }
+  static constexpr bool kHalfMajor = false;  // lane-major: lane l's 32 keys are contiguous
+  __device__ __forceinline__ int key_base(int64_t s) const { return static_cast<int>(s * STEP); }
+};
+
+template <class Src>
+__device__ __forceinline__ int compact_row(const Src& src, int64_t nsteps, int32_t* __restrict__ out,
+                                           int (*s_warp)[WARPS], uint16_t (*stage)[STEP]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int running = 0, rb = 0;
+  for (int64_t r0 = 0; r0 < nsteps; r0 += WARPS * SPW, rb ^= 1) {
+    const int64_t s0 = r0 + int64_t(warp) * SPW;
+    decltype(src.load(0)) d[SPW];
+#pragma unroll
+    for (int j = 0; j < SPW; ++j) d[j] = src.load(s0 + j);  // all loads in flight first
+    uint32_t m0[SPW], m1[SPW];
+    int o0[SPW], o1[SPW], tot[SPW], wsum = 0;
+#pragma unroll
+    for (int j = 0; j < SPW; ++j) {
+      src.masks(d[j], s0 + j, m0[j], m1[j]);
+      const int c0 = __popc(m0[j]), c1 = __popc(m1[j]);
+      const int packed = Src::kHalfMajor ? (c0 | (c1 << 16)) : c0 + c1;  // a half's sum <= 512
+      const int incl = warp_incl_scan(packed, lane);
+      const int t = __shfl_sync(0xffffffffu, incl, 31);
+      const int ex = incl - packed;
+      if (Src::kHalfMajor) {
+        o0[j] = ex & 0xFFFF;
+        o1[j] = (t & 0xFFFF) + (ex >> 16);
+        tot[j] = (t & 0xFFFF) + (t >> 16);
+      } else {
+        o0[j] = ex;
+        o1[j] = ex + c0;
+        tot[j] = t;
+      }
+      wsum += tot[j];
+    }
+    if (lane == 0) s_warp[rb][warp] = wsum;
+    __syncthreads();
+    int base = running, rtotal = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      const int v = s_warp[rb][w];
+      rtotal += v;
+      base += w < warp ? v : 0;
+    }
+    const int rel1 = Src::kHalfMajor ? STEP / 2 + lane * 16 : lane * 32 + 16;
+    const int rel0 = Src::kHalfMajor ? lane * 16 : lane * 32;
+#pragma unroll
+    for (int j = 0; j < SPW; ++j) {
+      uint16_t* st = stage[warp * 2 + (j & 1)];
+      emit16(st, o0[j], m0[j], rel0);
+      emit16(st, o1[j], m1[j], rel1);
+      __syncwarp();
+      const int kb = src.key_base(s0 + j);
+      for (int i = lane; i < tot[j]; i += 32) out[base + i] = kb + st[i];
+      base += tot[j];
+    }
+    running += rtotal;
+  }
+  return running;
+}
+
+__global__ void __launch_bounds__(WARPS * 32) fga_compact_kernel(const uint8_t* __restrict__ keep,
+                                                                const float* __restrict__ scores, int64_t n,
+                                                                int32_t* __restrict__ idx, int64_t stride,
+                                                                int32_t* __restrict__ counts, int fill) {
+  __shared__ int s_warp[2][WARPS];
+  __shared__ float s_bv[WARPS];
+  __shared__ int s_bi[WARPS];
+  __shared__ uint16_t s_stage[WARPS * 2][STEP];
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint8_t* kr = keep + row * n;
   int32_t* out = idx + row * stride;
   const int head = static_cast<int>(reinterpret_cast<uintptr_t>(kr) & 15u);
-  const uint8_t* abase = kr - head;  // 16-byte aligned
-  const int64_t span = head + n;
-  const int64_t nblk = (span + 15) >> 4;
-
-  // the next round's 16-byte block is loaded before this round's scan (two loads in flight)
-  auto load = [&](int64_t blk) -> uint4 {
-    const int64_t lo = blk * 16;
-    return (blk < nblk && lo >= head && lo + 16 <= span) ? __ldg(reinterpret_cast<const uint4*>(abase + lo))
-                                                         : make_uint4(0u, 0u, 0u, 0u);
-  };
-  uint4 wn = load(tid);
-  int running = 0;
-  for (int64_t b0 = 0; b0 < nblk; b0 += TC) {
-    const int64_t blk = b0 + tid;
-    const uint4 w = wn;
-    wn = load(blk + TC);
-    uint32_t bits = 0;
-    if (blk < nblk) {
-      const int64_t lo = blk * 16;
-      if (lo >= head && lo + 16 <= span) {
-        bits = nonzero_bytes(w.x) | (nonzero_bytes(w.y) << 4) | (nonzero_bytes(w.z) << 8) | (nonzero_bytes(w.w) << 12);
-      } else {
-#pragma unroll 4
-        for (int e = 0; e < 16; ++e) {
-          const int64_t pos = lo + e;
-          if (pos >= head && pos < span && abase[pos] != 0) bits |= 1u << e;
-        }
-      }
-    }
-    const int cnt = __popc(bits);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const int v = lane < WC ? s_warp[lane] : 0;
-      int sc = v;
-#pragma unroll
-      for (int o = 1; o < WC; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, sc, o);
-        if (lane >= o) sc += t;
-      }
-      if (lane < WC) s_warp[lane] = sc - v;  // exclusive warp prefix
-      if (lane == WC - 1) s_total = sc;
-    }
-    __syncthreads();
-    int off = s_warp[warp] + incl - cnt;
-    const int key0 = static_cast<int>(blk * 16 - head);
-    while (bits) {
-      s_stage[off++] = key0 + __ffs(bits) - 1;
-      bits &= bits - 1;
-    }
-    __syncthreads();
-    const int total = s_total;
-    for (int i = tid; i < total; i += TC) out[running + i] = s_stage[i];
-    running += total;
-    __syncthreads();
-  }
+  const ByteSrc src{kr - head, head, head + static_cast<int>(n), lane};
+  int running = compact_row(src, (head + n + STEP - 1) / STEP, out, s_warp, s_stage);
 
   if (running == 0 && scores != nullptr) {
     // argmax fallback, first maximum (np.argmax semantics)
     const float* sr = scores + row * n;
     float bv = -INFINITY;
     int bi = 0x7fffffff;
-    for (int64_t i = tid; i < n; i += TC) {
+    for (int64_t i = tid; i < n; i += WARPS * 32) {
       const float x = sr[i];
       if (x > bv || (x == bv && i < bi)) { bv = x; bi = static_cast<int>(i); }
     }
@@ -128,7 +209,7 @@ __global__ void __launch_bounds__(TC) fga_compact_kernel(const uint8_t* __restri
     if (lane == 0) { s_bv[warp] = bv; s_bi[warp] = bi; }
     __syncthreads();
     if (tid == 0) {
-      for (int w = 1; w < WC; ++w)
+      for (int w = 1; w < WARPS; ++w)
         if (s_bv[w] > bv || (s_bv[w] == bv && s_bi[w] < bi)) { bv = s_bv[w]; bi = s_bi[w]; }
       out[0] = bi == 0x7fffffff ? 0 : bi;  // all -inf / NaN rows: index 0 like np.argmax
     }
@@ -136,13 +217,13 @@ __global__ void __launch_bounds__(TC) fga_compact_kernel(const uint8_t* __restri
   }
   if (tid == 0) counts[row] = running;
   if (fill)
-    for (int64_t i = running + tid; i < n; i += TC) out[i] = -1;
+    for (int64_t i = running + tid; i < n; i += WARPS * 32) out[i] = -1;
 }
 
 // ---------------------------------------------------------------- bit-packed masks
-// keep bits: uint32 words, bit b of word w = key 32w + b.  Packing (one warp
-// ballot per 32 keys) and compaction from bits: each thread scans WPT words
-// per round, so a CTA covers 256 * WPT * 32 keys per round with one block scan.
+// keep bits: uint32 words, bit b of word w = key 32w + b.  Packing: one warp
+// ballot per 32 keys.  Compaction from bits: the same round schedule, lane l
+// holding word l of each 1024-key step (keys 32l .. 32l + 31).
 __global__ void __launch_bounds__(256) fga_pack_bits_kernel(const uint8_t* __restrict__ keep, int64_t rows, int64_t n,
                                                              int64_t words, uint32_t* __restrict__ bits) {
   const int lane = threadIdx.x & 31;
@@ -157,70 +238,20 @@ __global__ void __launch_bounds__(256) fga_pack_bits_kernel(const uint8_t* __res
   }
 }
 
-constexpr int WPT = 1;
-
-__global__ void __launch_bounds__(T) fga_compact_bits_kernel(const uint32_t* __restrict__ bits, int64_t words,
-                                                             int64_t n, int32_t* __restrict__ idx, int64_t stride,
-                                                             int32_t* __restrict__ counts, int fill) {
-  __shared__ int s_warp[W];
-  __shared__ int s_total;
-  __shared__ int s_stage[T * WPT * 32];
+__global__ void __launch_bounds__(WARPS * 32) fga_compact_bits_kernel(const uint32_t* __restrict__ bits, int64_t words,
+                                                                     int64_t n, int32_t* __restrict__ idx,
+                                                                     int64_t stride, int32_t* __restrict__ counts,
+                                                                     int fill) {
+  __shared__ int s_warp[2][WARPS];
+  __shared__ uint16_t s_stage[WARPS * 2][STEP];
   const int64_t row = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t* br = bits + row * words;
+  const int tid = threadIdx.x;
   int32_t* out = idx + row * stride;
-  int running = 0;
-  for (int64_t w0 = 0; w0 < words; w0 += int64_t(T) * WPT) {
-    uint32_t m[WPT];
-    int cnt = 0;
-#pragma unroll
-    for (int u = 0; u < WPT; ++u) {
-      const int64_t w = w0 + int64_t(tid) * WPT + u;
-      uint32_t v = w < words ? __ldg(br + w) : 0u;
-      const int64_t k0 = w * 32;
-      if (k0 + 32 > n) v &= (k0 >= n) ? 0u : ((1u << (n - k0)) - 1u);  // keys past n are not keys
-      m[u] = v;
-      cnt += __popc(v);
-    }
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const int v = lane < W ? s_warp[lane] : 0;
-      int sc = v;
-#pragma unroll
-      for (int o = 1; o < W; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, sc, o);
-        if (lane >= o) sc += t;
-      }
-      if (lane < W) s_warp[lane] = sc - v;
-      if (lane == W - 1) s_total = sc;
-    }
-    __syncthreads();
-    int off = s_warp[warp] + incl - cnt;
-#pragma unroll
-    for (int u = 0; u < WPT; ++u) {
-      uint32_t v = m[u];
-      const int key0 = static_cast<int>((w0 + int64_t(tid) * WPT + u) * 32);
-      while (v) {
-        s_stage[off++] = key0 + __ffs(v) - 1;
-        v &= v - 1;
-      }
-    }
-    __syncthreads();
-    const int total = s_total;
-    for (int i = tid; i < total; i += T) out[running + i] = s_stage[i];
-    running += total;
-    __syncthreads();
-  }
+  const BitSrc src{bits + row * words, words, n, tid & 31};
+  const int running = compact_row(src, (words + 31) / 32, out, s_warp, s_stage);
   if (tid == 0) counts[row] = running;
   if (fill)
-    for (int64_t i = running + tid; i < n; i += T) out[i] = -1;
+    for (int64_t i = running + tid; i < n; i += WARPS * 32) out[i] = -1;
 }
 
 }  // namespace
@@ -241,7 +272,7 @@ int launch_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* 
   if (n >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact_bits: n must be < 2^31");
   if (rows == 0) return FGA_OK;
   if (rows >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact_bits: too many rows");
-  fga_compact_bits_kernel<<<static_cast<unsigned>(rows), T, 0, stream>>>(bits, (n + 31) / 32, n, idx, idx_stride,
+  fga_compact_bits_kernel<<<static_cast<unsigned>(rows), WARPS * 32, 0, stream>>>(bits, (n + 31) / 32, n, idx, idx_stride,
                                                                            counts, fill);
   return check_launch("fga_compact_bits_kernel");
 }
@@ -252,7 +283,7 @@ int launch_compact(const uint8_t* keep, const float* scores, int64_t rows, int64
   if (n >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact: n must be < 2^31");
   if (rows == 0) return FGA_OK;
   if (rows >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact: too many rows");
-  fga_compact_kernel<<<static_cast<unsigned>(rows), TC, 0, stream>>>(keep, scores, n, idx, idx_stride, counts, fill);
+  fga_compact_kernel<<<static_cast<unsigned>(rows), WARPS * 32, 0, stream>>>(keep, scores, n, idx, idx_stride, counts, fill);
   return check_launch("fga_compact_kernel");
 }
 
