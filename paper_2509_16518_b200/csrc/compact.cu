@@ -32,8 +32,21 @@ namespace fga {
 namespace {
 
 constexpr int STEP = 1024;  // keys per warp step
-constexpr int WARPS = 8;
-constexpr int SPW = 4;      // steps per warp per round: a round is 32768 keys (c2's whole row)
+#ifndef FGA_CK_WARPS
+#define FGA_CK_WARPS 8
+#endif
+#ifndef FGA_CK_SPW
+#define FGA_CK_SPW 4
+#endif
+#ifndef FGA_CK_MINB
+#define FGA_CK_MINB 5
+#endif
+#ifndef FGA_CK_BUFS
+#define FGA_CK_BUFS 1
+#endif
+constexpr int WARPS = FGA_CK_WARPS;
+constexpr int SPW = FGA_CK_SPW;    // steps per warp per round: 8 x 4 steps = 32768 keys (c2's whole row)
+constexpr int BUFS = FGA_CK_BUFS;  // stage buffers per warp (1: an extra __syncwarp per step)
 
 // bit k of the result = (byte k of x != 0), k = 0..3
 __device__ __forceinline__ uint32_t nz4(uint32_t x) {
@@ -162,7 +175,8 @@ __device__ __forceinline__ int compact_row(const Src& src, int64_t nsteps, int32
     const int rel0 = Src::kHalfMajor ? lane * 16 : lane * 32;
 #pragma unroll
     for (int j = 0; j < SPW; ++j) {
-      uint16_t* st = stage[warp * 2 + (j & 1)];
+      uint16_t* st = stage[warp * BUFS + (j % BUFS)];
+      if (BUFS == 1 && j > 0) __syncwarp();  // the previous step's flush has read the stage
       emit16(st, o0[j], m0[j], rel0);
       emit16(st, o1[j], m1[j], rel1);
       __syncwarp();
@@ -175,14 +189,14 @@ __device__ __forceinline__ int compact_row(const Src& src, int64_t nsteps, int32
   return running;
 }
 
-__global__ void __launch_bounds__(WARPS * 32) fga_compact_kernel(const uint8_t* __restrict__ keep,
+__global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_kernel(const uint8_t* __restrict__ keep,
                                                                 const float* __restrict__ scores, int64_t n,
                                                                 int32_t* __restrict__ idx, int64_t stride,
                                                                 int32_t* __restrict__ counts, int fill) {
   __shared__ int s_warp[2][WARPS];
   __shared__ float s_bv[WARPS];
   __shared__ int s_bi[WARPS];
-  __shared__ uint16_t s_stage[WARPS * 2][STEP];
+  __shared__ uint16_t s_stage[WARPS * BUFS][STEP];
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint8_t* kr = keep + row * n;
@@ -238,12 +252,12 @@ __global__ void __launch_bounds__(256) fga_pack_bits_kernel(const uint8_t* __res
   }
 }
 
-__global__ void __launch_bounds__(WARPS * 32) fga_compact_bits_kernel(const uint32_t* __restrict__ bits, int64_t words,
+__global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_bits_kernel(const uint32_t* __restrict__ bits, int64_t words,
                                                                      int64_t n, int32_t* __restrict__ idx,
                                                                      int64_t stride, int32_t* __restrict__ counts,
                                                                      int fill) {
   __shared__ int s_warp[2][WARPS];
-  __shared__ uint16_t s_stage[WARPS * 2][STEP];
+  __shared__ uint16_t s_stage[WARPS * BUFS][STEP];
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x;
   int32_t* out = idx + row * stride;
