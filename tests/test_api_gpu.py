@@ -172,14 +172,20 @@ def test_sharded_tile_ranges_reassemble_bitwise():
 
 def test_bit_packed_compaction_matches_bytes():
     rng = np.random.default_rng(7)
-    for n in (1000, 4096, 33):
-        g = -(-n // 16)
-        keep = torch.from_numpy((rng.random((1, 2, g, n)) < 0.37).astype(np.uint8)).cuda()
+    for n, m in ((1000, 16), (4096, 16), (33, 16), (40001, 10000), (75600, 20000)):  # the last two: several rounds
+        g = -(-n // m)
+        keep_np = (rng.random((1, 2, g, n)) < 0.37).astype(np.uint8)
+        keep = torch.from_numpy(keep_np).cuda()
         bits = fga.pack_keep_bits(keep)
         assert bits.shape == (1, 2, g, (n + 31) // 32)
-        a = fga.compact_keep(keep, 16, fill_sentinel=True)
-        b = fga.compact_keep_bits(bits, 16, n, fill_sentinel=True)
+        a = fga.compact_keep(keep, m, fill_sentinel=True)
+        b = fga.compact_keep_bits(bits, m, n, fill_sentinel=True)
         assert torch.equal(a.idx, b.idx) and torch.equal(a.counts, b.counts)
+        got = a.idx.cpu().numpy()
+        for h in range(2):
+            for gi in range(g):
+                pos = np.flatnonzero(keep_np[0, h, gi])
+                assert np.array_equal(got[0, h, gi, : pos.size], pos) and (got[0, h, gi, pos.size:] == -1).all()
 
 
 def test_host_pipeline_equals_device_path():

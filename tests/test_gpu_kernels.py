@@ -69,7 +69,7 @@ def test_gather_rows_bitwise(d, n_idx):
 
 # ------------------------------------------------------------------ K1b compaction
 
-@pytest.mark.parametrize("n", [33, 1000, 4096, 32760])
+@pytest.mark.parametrize("n", [33, 1000, 4096, 32760, 40001, 75600])
 @pytest.mark.parametrize("fill", [0, 1])
 def test_compact_bit_exact(n, fill):
     rng = np.random.default_rng(n)
