@@ -235,6 +235,11 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
         }
         epi_bar();
       }
+      float nz[32];  // pass 1: -(m_i + ln den_i) of this warp's 32 queries, in registers for the unit
+      if (PASS == 1) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) nz[k] = -tab[w * 32 + k].z;
+      }
       float m = -INFINITY;
       double den = 0.0;
       for (int c = c_lo; c < c_hi; ++c, ++sc) {
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
           int bi = 0;
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            const float y = fmaf(__uint_as_float(v[k]), p.scale, -tab[w * 32 + k].z);
+            const float y = fmaf(__uint_as_float(v[k]), p.scale, nz[k]);
             if (y > by) {
               by = y;
               bacc = __uint_as_float(v[k]);
