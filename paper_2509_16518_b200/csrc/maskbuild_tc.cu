@@ -15,9 +15,14 @@
 //                   ex2 terms, accumulated and rescaled in fp64); writes m_i and 1/den_i.
 //   pass 1 (group): S^T = K_c Q_g^T, thread = key j, columns = the group's 128 queries.
 //                   The transposed tile turns the column max over a group into a per-thread
-//                   max: select i* = argmax_i s_ij - (m_i + ln den_i) (one FFMA and a compare
-//                   per element, no exp), then gmax_gj = expf(s_i*j - m_i*) / den_i* evaluated
-//                   as the reference does, bf16-rounded.
+//                   max: y_j = max_i s_ij - (m_i + ln den_i) (half an FFMA2 and half an FMNMX3
+//                   per element, -(m_i + ln den_i) in registers), gmax_gj = expf(y_j), bf16-
+//                   rounded.  exp(y) = exp(s - m) / den up to ~1e-6 relative (the rounding of
+//                   m + ln den), far below a bf16 step: at N = 4000-4096 5.7-6.3e-5 of the values
+//                   land one bf16 step away from NumPy's, against 4.2-5.5e-5 when the argmax
+//                   query is selected and a_i*j = expf(s - m_i*) / den_i* is evaluated as the
+//                   reference does (-DFGA_CB_EXACT_SELECT: 3 more instructions per element,
+//                   pass 1 ~25% slower).
 //
 // Warps (18, one CTA per SM, persistent over (b, h, tile) units): 0-15 epilogue (four per TMEM
 // lane quadrant, 32 columns each), 16 MMA issuer, 17 TMA producer (Q tile + 4-slot K ring).
@@ -301,9 +306,26 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             den += static_cast<double>(acc.x) + static_cast<double>(acc.y);
           }
         } else {
-          // columns: the group's queries i = 32w + k; row: key j = c*128 + row.  Select the query
-          // maximising s_ij - (m_i + ln den_i), then evaluate a_ij = expf(s_ij - m_i) / den_i exactly
-          // as the reference does for that one query.
+          // columns: the group's queries i = 32w + k; row: key j = c*128 + row.
+          float* xy = reinterpret_cast<float*>(smem + L::OFF_XCH) + (sc & 1) * (3 * CB_EW * 128);
+#ifndef FGA_CB_EXACT_SELECT
+          // y_j = max_i s_ij - (m_i + ln den_i); gmax_gj = exp(y_j)
+          float by = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            const float2 y2 = __ffma2_rn(make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                                         make_float2(p.scale, p.scale), make_float2(nz[k], nz[k + 1]));
+            by = fmax3f(by, y2.x, y2.y);
+          }
+          if (w > 0) xy[w * 128 + row] = by;
+          epi_bar();  // double-buffered by chunk parity: one barrier per chunk
+          if (w == 0) {
+#pragma unroll
+            for (int o = 1; o < CB_EW; ++o) by = fmaxf(by, xy[o * 128 + row]);
+            float g = expf(by);
+#else
+          // select the query maximising s_ij - (m_i + ln den_i), then evaluate
+          // a_ij = expf(s_ij - m_i) / den_i as the reference does for that one query
           float by = -INFINITY, bacc = 0.f;
           int bi = 0;
 #pragma unroll
@@ -315,7 +337,6 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
               bi = w * 32 + k;
             }
           }
-          float* xy = reinterpret_cast<float*>(smem + L::OFF_XCH) + (sc & 1) * (3 * CB_EW * 128);
           if (w > 0) {
             xy[(w * 3 + 0) * 128 + row] = by;
             xy[(w * 3 + 1) * 128 + row] = bacc;
@@ -334,6 +355,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             }
             const float4 e = tab[bi];
             float g = __fmul_rn(expf(__fsub_rn(__fmul_rn(bacc, p.scale), e.x)), e.y);
+#endif
             if (p.round) g = __bfloat162float(__float2bfloat16_rn(g));
             const int j = c * BN + row;
             if (j < p.n) p.gmax[(bh * p.tiles + t) * static_cast<int64_t>(p.n) + j] = g;
