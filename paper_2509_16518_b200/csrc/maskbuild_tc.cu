@@ -38,6 +38,10 @@
 namespace fga {
 namespace {
 
+#ifndef FGA_CB_POLY
+#define FGA_CB_POLY 0
+#endif
+constexpr int CB_POLY = FGA_CB_POLY;  // pass 0: every CB_POLY-th pair of exps on the FMA pipe (0: none)
 constexpr int CB_EW = 4;              // epilogue warps per TMEM lane quadrant
 constexpr int CB_EPI = 4 * CB_EW;      // epilogue warps 0..15
 constexpr int CB_WARPS = CB_EPI + 2;   // + MMA issuer + TMA producer
@@ -301,7 +305,10 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             for (int k = 0; k < 32; k += 2) {
               const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
                                           make_float2(sl, sl), make_float2(-ml, -ml));
-              acc = __fadd2_rn(acc, make_float2(ex2(x.x), ex2(x.y)));
+              if (CB_POLY > 0 && (k / 2) % CB_POLY == CB_POLY - 1)
+                acc = __fadd2_rn(acc, ex2_poly2<5>(x));  // this pair on the FMA pipe
+              else
+                acc = __fadd2_rn(acc, make_float2(ex2(x.x), ex2(x.y)));
             }
             den += static_cast<double>(acc.x) + static_cast<double>(acc.y);
           }

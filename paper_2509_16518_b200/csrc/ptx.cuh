@@ -332,7 +332,14 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 u = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
   const float2 f = __ffma2_rn(u, make_float2(-1.f, -1.f), x);  // x - round(x)
   float2 p;
-  if constexpr (DEG == 3) {  // max rel. error 1.0e-4
+  if constexpr (DEG == 5) {  // max rel. error 2.2e-7 in fp32 (about ex2.approx's own)
+    p = __ffma2_rn(f, make_float2(0.0013266970636323094f, 0.0013266970636323094f),
+                   make_float2(0.009675459936261177f, 0.009675459936261177f));
+    p = __ffma2_rn(p, f, make_float2(0.05550742521882057f, 0.05550742521882057f));
+    p = __ffma2_rn(p, f, make_float2(0.24022121727466583f, 0.24022121727466583f));
+    p = __ffma2_rn(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
+    p = __ffma2_rn(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  } else if constexpr (DEG == 3) {  // max rel. error 1.0e-4
     p = __ffma2_rn(f, make_float2(0.0550141495f, 0.0550141495f), make_float2(0.2422112540f, 0.2422112540f));
     p = __ffma2_rn(p, f, make_float2(0.6932820230f, 0.6932820230f));
     p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
