@@ -469,7 +469,7 @@ def e2e_leg(args, torch, fga, cfg, q, k, v, keep, out, flops, flush, stream, wor
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": out.numel() * 2, "ranks": world,
             "path": "sparse_attention_host: pinned host Q/K/V + bit-packed slice mask -> H2D | "
                     "fga_compact_bits + fga_sparse_attn_fwd | D2H, overlapped over 5 head slabs (the last one a "
-                    "single head); every rank at once, max time over ranks",
+                    "single head, its query groups in 2 runs); every rank at once, max time over ranks",
             "max_abs_diff_vs_device_path": e2e_err}
 
 

@@ -36,7 +36,7 @@ def pack_keep_bits(keep):
 class HostPipeline:
     """Device buffers + streams for one problem shape (reused across calls)."""
 
-    def __init__(self, cfg: AttnConfig, slabs: int = 4, device=None, tail: bool = True):
+    def __init__(self, cfg: AttnConfig, slabs: int = 4, device=None, tail: bool = True, tail_parts: int = 2):
         t = torch()
         self.dev = require_device(device)
         self.cfg = cfg
@@ -56,6 +56,12 @@ class HostPipeline:
         for sz in sizes:
             self.ranges.append((h0, h0 + sz))
             h0 += sz
+        # With a one-head tail, that head's K/V/bits go up first and its query groups in
+        # `tail_parts` runs (fga_sparse_attn_fwd_tiles), so only the last run's Q upload, one
+        # wave of tiles and the last run's D2H remain after the bulk of the PCIe traffic.
+        g = cfg.num_groups
+        parts = max(1, min(tail_parts, g)) if (sizes and sizes[-1] == 1 and len(sizes) > 1) else 1
+        self.tail_groups = [(g * i // parts, g * (i + 1) // parts) for i in range(parts)]
         n, d, g = cfg.seq_len, cfg.head_dim, cfg.num_groups
         self.words = (n + 31) // 32
         kw = dict(device=f"cuda:{self.dev}")
@@ -81,7 +87,32 @@ class HostPipeline:
         for s_ in (self.s_h2d, self.s_cmp, self.s_d2h):
             s_.wait_event(start)
         last = None
-        for h0, h1 in self.ranges:
+        m = cfg.group_size
+        tpg = -(-m // 128)  # work tiles per group
+        for si, (h0, h1) in enumerate(self.ranges):
+            if si == len(self.ranges) - 1 and len(self.tail_groups) > 1:
+                with t.cuda.stream(self.s_h2d):
+                    for dst, src in ((self.bits, hb), (self.k, hk), (self.v, hv)):
+                        dst[h0:h1].copy_(src[h0:h1], non_blocking=True)
+                sh = _lib.shape(1, 1, n, d, m, cfg.scale)
+                cs = self.s_cmp.cuda_stream
+                for g0, g1 in self.tail_groups:
+                    r0, r1 = g0 * m, min(g1 * m, n)
+                    with t.cuda.stream(self.s_h2d):
+                        self.q[h0, r0:r1].copy_(hq[h0, r0:r1], non_blocking=True)
+                        ev_in = self.s_h2d.record_event()
+                    self.s_cmp.wait_event(ev_in)
+                    _lib.call("fga_compact_bits", ptr(self.bits[h0, g0]), g1 - g0, n, ptr(self.idx[h0, g0]), n,
+                              ptr(self.counts[h0, g0]), 0, cs)
+                    _lib.call("fga_sparse_attn_fwd_tiles", ptr(self.q[h0]), ptr(self.k[h0]), ptr(self.v[h0]),
+                              ptr(self.idx[h0]), n, ptr(self.counts[h0]), ptr(self.o[h0]), _lib.FGA_OUT_BF16, None,
+                              sh, g0 * tpg, g1 * tpg, cs)
+                    ev_c = self.s_cmp.record_event()
+                    self.s_d2h.wait_event(ev_c)
+                    with t.cuda.stream(self.s_d2h):
+                        ho[h0, r0:r1].copy_(self.o[h0, r0:r1], non_blocking=True)
+                        last = self.s_d2h.record_event()
+                continue
             with t.cuda.stream(self.s_h2d):
                 for dst, src in ((self.bits, hb), (self.q, hq), (self.k, hk), (self.v, hv)):
                     dst[h0:h1].copy_(src[h0:h1], non_blocking=True)
@@ -108,7 +139,8 @@ class HostPipeline:
 _pipes: dict = {}
 
 
-def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: int = 5, tail: bool = True):
+def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: int = 5, tail: bool = True,
+                          tail_parts: int = 2):
     """FG-Attn from pinned host buffers (see module doc).  Returns the pinned host output;
     synchronise the current stream before reading it."""
     t = torch()
@@ -120,9 +152,9 @@ def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: 
     expect = (cfg.batch, cfg.heads, cfg.num_groups, (cfg.seq_len + 31) // 32)
     if tuple(keep_bits.shape) != expect:
         raise ShapeError(f"keep_bits must be {expect}, got {tuple(keep_bits.shape)}")
-    key = (cfg, slabs, tail, require_device())
+    key = (cfg, slabs, tail, tail_parts, require_device())
     if key not in _pipes:
-        _pipes[key] = HostPipeline(cfg, slabs, tail=tail)
+        _pipes[key] = HostPipeline(cfg, slabs, tail=tail, tail_parts=tail_parts)
     if out is None:
         out = t.empty(cfg.dims, dtype=t.bfloat16, pin_memory=True)
     return _pipes[key](q, k, v, keep_bits, out)

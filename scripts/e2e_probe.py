@@ -17,15 +17,17 @@ hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
 hb = bits.cpu().pin_memory()
 ho = torch.empty(cfg.dims, dtype=torch.bfloat16).pin_memory()
 for spec in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["4", "6", "12"]):
-    slabs, tail = int(spec.rstrip("u")), not spec.endswith("u")  # "6u": uniform slabs
+    # "6u": uniform slabs; "5p4": 5 slabs, the one-head tail slab in 4 query-group runs
+    base, _, parts = spec.rstrip("u").partition("p")
+    slabs, tail, parts = int(base), not spec.endswith("u"), int(parts or 2)
     for _ in range(3):
-        fga.sparse_attention_host(hq, hk, hv, hb, cfg, out=ho, slabs=slabs, tail=tail)
+        fga.sparse_attention_host(hq, hk, hv, hb, cfg, out=ho, slabs=slabs, tail=tail, tail_parts=parts)
     torch.cuda.synchronize()
     ts = []
     for _ in range(10):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fga.sparse_attention_host(hq, hk, hv, hb, cfg, out=ho, slabs=slabs, tail=tail)
+        fga.sparse_attention_host(hq, hk, hv, hb, cfg, out=ho, slabs=slabs, tail=tail, tail_parts=parts)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
