@@ -201,6 +201,20 @@ def test_host_pipeline_equals_device_path():
         assert torch.equal(out, ref.cpu()), slabs
 
 
+def test_host_pipeline_split_tail_ragged():
+    # ragged N (short last group) with the one-head tail slab in 1..5 query-group runs
+    cfg = fga.AttnConfig(1, 4, 2000, 128)
+    q, k, v = (torch.randn(cfg.dims, device="cuda").to(torch.bfloat16) for _ in range(3))
+    keep = (torch.rand((1, 4, cfg.num_groups, cfg.seq_len), device="cuda") < 0.4).to(torch.uint8)
+    ref = fga.sparse_attention(q, k, v, fga.compact_keep(keep, 128), cfg).cpu()
+    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+    hb = fga.pack_keep_bits(keep).cpu().pin_memory()
+    for parts in (1, 3, 5):
+        out = fga.sparse_attention_host(hq, hk, hv, hb, cfg, slabs=3, tail_parts=parts)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), parts
+
+
 def test_sparse_attention_is_bitwise_reproducible():
     # the two MMA issuers issue their PVs in chunk order (FGA_PV_ORDER), so O accumulates the
     # chunks in list order on every run (without it ~1e-6 of the outputs flip between runs)
