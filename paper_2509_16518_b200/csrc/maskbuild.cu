@@ -191,6 +191,10 @@ constexpr int TK_BINS = 4096;
 #define FGA_TOPK_EQ_MAX 256
 #endif
 constexpr int TK_EQ_MAX = FGA_TOPK_EQ_MAX > 0 ? FGA_TOPK_EQ_MAX : 1;  // ties at the threshold resolved by rank counting up to this many
+#ifndef FGA_TOPK_ORD_N
+#define FGA_TOPK_ORD_N 81920
+#endif
+constexpr int TK_ORD_N = FGA_TOPK_ORD_N;  // rows up to this long resolve many ties with one block scan
 template <typename Keys>
 __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t k, uint8_t* __restrict__ keep) {
   __shared__ uint32_t hist[TK_BINS];
@@ -201,6 +205,8 @@ __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t 
   __shared__ int s_tot;
   __shared__ int64_t s_eqcnt;
   __shared__ int s_eqidx[TK_EQ_MAX];
+  __shared__ uint32_t s_ordmask[TK_ORD_N / 32];  // per (512-key iteration, warp): ballot of tied keys
+  __shared__ int s_ordcnt[TK_ORD_N / 32];        // its popcount, then its exclusive rank base
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t prefix = 0, mask = 0;
@@ -280,6 +286,54 @@ __global__ void __launch_bounds__(TK) topk_kernel(Keys keys, int64_t n, int64_t 
       int rank = 0;
       for (int f = 0; f < n_eq; ++f) rank += s_eqidx[f] < me;
       if (rank < rem) keep[row * n + me] = 1;
+    }
+    return;
+  }
+  if (n <= TK_ORD_N) {
+    // many ties: one coalesced pass keeps the larger keys and records, per (iteration, warp),
+    // the ballot of keys equal to the threshold; one block scan over those counts in index
+    // order gives every tied key its rank; the first `rem` of them are kept.
+    const int nit = static_cast<int>((n + TK - 1) / TK);
+    for (int it = 0; it < nit; ++it) {
+      const int64_t i = static_cast<int64_t>(it) * TK + tid;
+      uint32_t key = 0;
+      if (i < n) key = keys(row, n, i);
+      const bool eq = i < n && key == prefix;
+      const unsigned bal = __ballot_sync(0xffffffffu, eq);
+      if (i < n) keep[row * n + i] = key > prefix ? 1 : 0;
+      if (lane == 0) {
+        s_ordmask[it * (TK / 32) + warp] = bal;
+        s_ordcnt[it * (TK / 32) + warp] = __popc(bal);
+      }
+    }
+    __syncthreads();
+    // exclusive scan of the nit * (TK/32) counts (iteration-major = index order)
+    const int ne = nit * (TK / 32);
+    const int per = (ne + TK - 1) / TK;
+    int own = 0;
+    for (int e = tid * per; e < min(ne, tid * per + per); ++e) own += s_ordcnt[e];
+    int incl = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int run = incl - own;
+    for (int w = 0; w < warp; ++w) run += s_warp[w];
+    for (int e = tid * per; e < min(ne, tid * per + per); ++e) {
+      const int c = s_ordcnt[e];
+      s_ordcnt[e] = run;
+      run += c;
+    }
+    __syncthreads();
+    for (int it = 0; it < nit; ++it) {
+      const uint32_t m = s_ordmask[it * (TK / 32) + warp];
+      if ((m >> lane) & 1u) {
+        const int rank = s_ordcnt[it * (TK / 32) + warp] + __popc(m & ((1u << lane) - 1u));
+        if (rank < rem) keep[row * n + static_cast<int64_t>(it) * TK + tid] = 1;
+      }
     }
     return;
   }

@@ -447,3 +447,25 @@ def test_cached_group_max_tensor_cores_mismatch_rate_large(n, cc, monkeypatch):
         rel = np.abs(got[mism] - ref[mism]) / np.maximum(np.abs(ref[mism]), 1e-30)
         assert rel.max() <= 2 ** -7
     assert (((got >= 0.5 / n) != keep_ref) <= mism).all()
+
+
+@pytest.mark.parametrize("n,distinct", [(5000, 7), (32760, 300), (40000, 3), (90000, 5)])
+def test_topk_keep_many_ties(n, distinct):
+    # rows whose k-th largest value is shared by hundreds to thousands of keys (the builders'
+    # bf16-valued scores): exactly k kept, ties toward the smaller index (masks.py:144-145,
+    # lexsort((arange, -s))); n = 90000 takes the long-row ordered pass
+    rng = np.random.default_rng(n)
+    rows = 6
+    vals = rng.standard_normal(distinct).astype(np.float32)
+    scores = vals[rng.integers(0, distinct, size=(rows, n))]
+    keep = torch.empty((rows, n), dtype=torch.uint8, device="cuda")
+    sd = torch.from_numpy(scores).cuda()
+    for k in (1, n // 3, n // 2 + 7, n - 1):
+        _lib.call("fga_topk_keep", ptr(sd), rows, n, k, ptr(keep), stream())
+        torch.cuda.synchronize()
+        got = keep.cpu().numpy()
+        for r in range(rows):
+            order = np.lexsort((np.arange(n), -scores[r]))[:k]
+            ref = np.zeros(n, np.uint8)
+            ref[order] = 1
+            assert np.array_equal(got[r], ref), (n, k, r)
