@@ -18,8 +18,10 @@
 // independent, so they overlap.  One __syncthreads per round exchanges the
 // warp totals.  Each lane then emits its kept positions into its warp's
 // shared-memory stage with an unrolled predicated loop (no divergence) and
-// after a __syncwarp the warp writes the step's positions out coalesced; the
-// stage is double-buffered per warp so that is the only synchronisation.
+// after a __syncwarp the warp writes the step's positions out coalesced (one
+// 2 KB stage per warp and a second __syncwarp before the next step's emission:
+// 16 KB per CTA and <= 48 registers give 5 CTAs per SM, faster than a
+// double-buffered stage at 4 CTAs; FGA_CK_BUFS=2).
 // Positions come out ascending, bit-exact with np.nonzero, with no sort.
 // HBM-bound: read n bytes (n/8 for bits), write 4*count (+4*(n-count)).
 // (Round-1 history: a block scan per 16 keys per thread was issue-bound at 80%
@@ -39,7 +41,7 @@ constexpr int STEP = 1024;  // keys per warp step
 #define FGA_CK_SPW 4
 #endif
 #ifndef FGA_CK_MINB
-#define FGA_CK_MINB 5
+#define FGA_CK_MINB 5  // min CTAs per SM for __launch_bounds__ (caps registers at 48)
 #endif
 #ifndef FGA_CK_BUFS
 #define FGA_CK_BUFS 1
