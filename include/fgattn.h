@@ -100,12 +100,16 @@ int fga_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, i
  * online softmax of tiled.py:48-77; equals oracle.py:55-82
  * (masked_dense_attention) within bf16 tolerance.
  *   idx    : int32, row (b,h,g) at idx + ((b*H+h)*G+g)*idx_group_stride,
- *            ascending or not, first counts[(b*H+h)*G+g] entries used; all
- *            entries must lie in [0, N) (checked by the Python mirror).
- *   counts : int32 [B*H*G], each >= 1.
+ *            first counts[(b*H+h)*G+g] entries used (ascending, as
+ *            SparseIndexMask keeps them).
+ *   counts : int32 [B*H*G], each in [1, idx_group_stride].
  *   o      : [B, H, N, D], bf16 (o_dtype = FGA_OUT_BF16) or fp32 (FGA_OUT_F32).
  *   lse    : optional fp32 [B, H, N] natural-log softmax normaliser.
  * Supported: head_dim in {64, 128}; any group_size in [1, N].
+ * Masks that break the invariants never make the kernels read out of bounds
+ * (counts are clamped to [0, stride], out-of-range keys read row 0) but give
+ * unspecified rows; fga_validate_mask or the FGA_ATTN_CHECK flag of
+ * fga_sparse_attn_fwd_ex report them as the reference does (sparse.py:47-52).
  */
 int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32_t* idx,
                         int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
@@ -121,6 +125,50 @@ int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32
 int fga_sparse_attn_fwd_tiles(const void* q, const void* k, const void* v, const int32_t* idx,
                               int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
                               fga_shape shape, int64_t tile_begin, int64_t tile_end, void* stream);
+
+/* Mask-violation bits written to a status word (int32[2] device workspace:
+ * [0] = OR of the bits, [1] = first offending row when known). */
+#define FGA_STATUS_EMPTY 1   /* a group with count < 1        (sparse.py:47-48) */
+#define FGA_STATUS_RANGE 2   /* a key outside [0, N)          (sparse.py:49-52) */
+#define FGA_STATUS_STRIDE 4  /* count > idx_group_stride                        */
+#define FGA_STATUS_ORDER 8   /* list not strictly ascending (fga_validate_mask) */
+
+/* fga_sparse_attn_fwd_ex flags */
+#define FGA_ATTN_CHECK 1     /* reset *status, run, synchronise, return FGA_EINVAL / FGA_ERANGE on violations */
+#define FGA_ATTN_PER_TILE 2  /* per-tile kernel also for 129..256-row groups (no shared-gather dual kernel)  */
+#define FGA_ATTN_STATIC 4    /* static tile stride instead of the dynamic tile scheduler                     */
+
+/*
+ * General form of the two entries above.
+ *   order  : optional int32 [tile_end - tile_begin]: the k-th tile claimed is
+ *            tile_begin + order[k] (a permutation; e.g. longest lists first
+ *            within each head, see fga_tile_order).  NULL = ascending.
+ *   status : optional int32[2] device word; the kernel ORs FGA_STATUS_* bits
+ *            into status[0] (the caller zeroes it, unless FGA_ATTN_CHECK).
+ *   flags  : FGA_ATTN_* bits.
+ */
+int fga_sparse_attn_fwd_ex(const void* q, const void* k, const void* v, const int32_t* idx,
+                           int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
+                           fga_shape shape, int64_t tile_begin, int64_t tile_end, const int32_t* order,
+                           int32_t* status, int flags, void* stream);
+
+/*
+ * Checks an index mask against the SparseIndexMask invariants
+ * (sparse.py:36-52): 1 <= counts[r] <= idx_group_stride, keys in [0, n),
+ * strictly ascending.  Synchronises `stream`; returns FGA_OK, FGA_EINVAL
+ * (count or order) or FGA_ERANGE (key range).  status: int32[2] device
+ * workspace (left holding the bits and the first offending row).
+ */
+int fga_validate_mask(const int32_t* idx, int64_t idx_group_stride, const int32_t* counts, int64_t rows, int64_t n,
+                      int32_t* status, void* stream);
+
+/*
+ * Longest-first tile order for fga_sparse_attn_fwd_ex: within each head
+ * (b,h), its groups' tiles sorted by list length, descending (ties by group
+ * index); heads stay in order, so the K/V of about two heads are live in L2
+ * at a time.  order: int32 [B*H*G*ceil(M/128)].
+ */
+int fga_tile_order(const int32_t* counts, fga_shape shape, int32_t* order, void* stream);
 
 /*
  * Dense attention with the same kernel and contiguous key chunks (every group

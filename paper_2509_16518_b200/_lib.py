@@ -17,6 +17,8 @@ LIB_PATH = os.environ.get("FGA_LIB") or os.path.join(_HERE, "libfgattn.so")  # F
 
 FGA_OK, FGA_EINVAL, FGA_ERANGE, FGA_ECUDA, FGA_EUNSUPPORTED = 0, -1, -2, -3, -4
 FGA_OUT_BF16, FGA_OUT_F32 = 0, 1
+FGA_STATUS_EMPTY, FGA_STATUS_RANGE, FGA_STATUS_STRIDE, FGA_STATUS_ORDER = 1, 2, 4, 8
+FGA_ATTN_CHECK, FGA_ATTN_PER_TILE, FGA_ATTN_STATIC = 1, 2, 4
 
 
 class FgaShape(ctypes.Structure):
@@ -39,6 +41,9 @@ _SIGS = {
     "fga_fgm1_unpack": ([_P, _P, _I64, _I64, _P, _I64, _P, _I, _P], _I),
     "fga_sparse_attn_fwd": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _P], _I),
     "fga_sparse_attn_fwd_tiles": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _I64, _I64, _P], _I),
+    "fga_sparse_attn_fwd_ex": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _I64, _I64, _P, _P, _I, _P], _I),
+    "fga_validate_mask": ([_P, _I64, _P, _I64, _I64, _P, _P], _I),
+    "fga_tile_order": ([_P, FgaShape, _P, _P], _I),
     "fga_dense_attn_fwd": ([_P, _P, _P, _P, _I, _P, FgaShape, _P], _I),
     "fga_gather_rows": ([_P, _I64, _I64, _P, _I64, _P, _P], _I),
     "fga_pooled_scores": ([_P, _P, FgaShape, _I, _P, _P], _I),
@@ -86,6 +91,12 @@ def check(rc: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def call_rc(name: str, *args) -> tuple[int, str]:
+    """Raw return code and message, for callers that map codes themselves."""
+    rc = getattr(load(), name)(*args)
+    return rc, ("" if rc == FGA_OK else load().fga_last_error().decode(errors="replace"))
 
 
 def shape(batch, heads, seq_len, head_dim, group_size, scale=None) -> FgaShape:

@@ -6,6 +6,7 @@
 
 #include <cstdint>
 
+#include "../../include/fgattn.h"
 #include "ptx.cuh"
 
 namespace fga {
@@ -29,7 +30,14 @@ struct AttnParams {
   int dense;
   long long* trace;  // debug timeline (FGA_TRACE=<file>): CTA 0, tile iteration trace_it, clock64 per phase
   int trace_it;      // FGA_TRACE_IT (default 0)
+  int32_t* status;       // nullable device word: FGA_STATUS_* bits of mask violations seen (atomicOr)
+  unsigned int* sched;   // dynamic tile counter (self-resetting, attn_ws.cu); null = static stride
+  const int32_t* order;  // nullable: work index -> tile offset from tile_begin (LPT order)
 };
+
+// Mask violations the kernels detect while running are ORed into p.status as the FGA_STATUS_*
+// bits of fgattn.h (sparse.py:47-52 raises for these).  The kernels stay memory-safe: counts are
+// clamped to [0, stride] and out-of-range keys read row 0.
 
 // Debug timeline hooks (FGA_TRACE=<file>).  Chunk level: slot s of chunk j
 // (j < 64) of CTA 0's tile iteration p.trace_it.  Tile level: slot s of CTA 0's
@@ -81,8 +89,9 @@ struct Tile {
   int q0;       // first query row within the head
   int rows;     // valid query rows in this tile
   int row0;     // first row of head (b,h) in the [B*H*N, D] view
-  int count;    // keys in the list
+  int count;    // keys in the list (clamped to [0, stride])
   int nchunks;  // ceil(count / BN)
+  int32_t bad;  // FGA_STATUS_* bits of this tile's count
   const int32_t* list;
 };
 
@@ -96,7 +105,14 @@ __device__ __forceinline__ Tile decode_tile(const AttnParams& p, int64_t tile) {
   const int q_end = min(g * p.group_size + p.group_size, p.seq_len);
   t.rows = min(BM, q_end - t.q0);
   t.row0 = static_cast<int>(bh * p.seq_len);
-  t.count = p.dense ? p.seq_len : __ldg(p.counts + t.bhg);
+  t.bad = 0;
+  if (p.dense) {
+    t.count = p.seq_len;
+  } else {
+    const int c = __ldg(p.counts + t.bhg);
+    t.bad = (c < 1 ? FGA_STATUS_EMPTY : 0) | (c > p.idx_group_stride ? FGA_STATUS_STRIDE : 0);
+    t.count = static_cast<int>(min(static_cast<int64_t>(max(c, 0)), p.idx_group_stride));
+  }
   t.nchunks = (t.count + BN - 1) / BN;
   t.list = p.dense ? nullptr : p.idx + t.bhg * p.idx_group_stride;
   return t;
@@ -129,7 +145,24 @@ __device__ __forceinline__ void store_row32(void* out, int64_t off, const uint32
 int launch_attn_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, int d, bool out_f32,
                    cudaStream_t stream);
 int launch_attn_dual(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
-int launch_attn_pp(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
-int launch_attn_sync(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
+
+// Producer-side mask checks.  load_key returns list[row] for row < count, else -1 (zero-fill);
+// a listed key outside [0, N) is replaced by row 0 (never read out of bounds) and flagged, and
+// report_keys() ORs FGA_STATUS_RANGE into p.status once per warp; report_tile() adds a tile's
+// count violations.
+__device__ __forceinline__ int load_key(const AttnParams& p, const int32_t* list, int row, int count, bool& oor) {
+  if (row >= count) return -1;
+  const int key = __ldg(list + row);
+  if (static_cast<unsigned>(key) < static_cast<unsigned>(p.seq_len)) return key;
+  oor = true;
+  return 0;
+}
+__device__ __forceinline__ void report_keys(const AttnParams& p, bool oor) {
+  if (__any_sync(0xffffffffu, oor) && p.status != nullptr && (threadIdx.x & 31) == 0)
+    atomicOr(p.status, FGA_STATUS_RANGE);
+}
+__device__ __forceinline__ void report_tile(const AttnParams& p, const Tile& t) {
+  if (t.bad && p.status != nullptr) atomicOr(p.status, t.bad);
+}
 
 }  // namespace fga

@@ -14,7 +14,8 @@
 // TMEM (512 columns): O_0 | O_1 | S_0,0 S_0,1 | S_1,0 S_1,1 (64 columns each); each tile keeps its
 // own running max and accumulator, so the epilogues need no exchange.  The two halves are two
 // chains per tile (S_c+1,h reuses the buffer PV_c,h reads, issued right behind it), and the two
-// warpgroups take turns on each sub-partition's MUFU (attn_pp.cu's named-barrier turns) so one
+// warpgroups take turns on each sub-partition's MUFU (named-barrier turns, as in the ping-pong
+// kernel of round 1, git history) so one
 // exponentiates while the tensor core serves the other.  Default for 129..256-row groups
 // (1-7% faster than attn_ws.cu there).
 //
@@ -116,15 +117,15 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem
   uint32_t item = 0;
   for (int64_t u = blockIdx.x; u < n_groups(p); u += gridDim.x) {
     const Tile t = group_tile(p, u, 0);
+    if (kv == 0 && part == 0 && lane == 0) report_tile(p, t);
     const char* gsrc = static_cast<const char*>(kv ? p.v : p.k) + static_cast<int64_t>(t.row0) * (D * 2) + ch * 16;
     for (int c = 0; c < t.nchunks; ++c, ++item) {
       const uint32_t slot = item % nslot, use = item / nslot;
       int keys[ROWS / 32];
+      bool oor = false;
 #pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) {
-        const int row = c * BN + part * ROWS + i * 32 + lane;
-        keys[i] = row < t.count ? __ldg(t.list + row) : -1;
-      }
+      for (int i = 0; i < ROWS / 32; ++i) keys[i] = load_key(p, t.list, c * BN + part * ROWS + i * 32 + lane, t.count, oor);
+      report_keys(p, oor);
       mbar_wait(&emptyb[slot], (use & 1) ^ 1);          // tile 0's reads of the slot done
       mbar_wait(&emptyb[nslot + slot], (use & 1) ^ 1);  // and tile 1's
       // this thread's copies into the slot's previous use completed before the slot filled (the
@@ -500,11 +501,9 @@ template <int D, bool F32>
 int launch_dual(const CUtensorMap* maps, const AttnParams& p, cudaStream_t stream) {
   auto kern = fga_attn_dual_kernel<D, F32>;
   const int smem = DuSmem<D>::BYTES;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return check_launch("cudaFuncSetAttribute(attn_dual)");
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const int rc = smem_opt_in(reinterpret_cast<const void*>(kern), smem, "attn_dual"); rc != FGA_OK)
+    return rc;
+  const int sms = sm_count();
   const int64_t groups = (p.n_tiles - p.tile_begin) / 2;
   const int64_t grid = groups < sms ? groups : sms;
   kern<<<static_cast<unsigned>(grid), 32 * NWARPS, smem, stream>>>(maps[0], p);

@@ -26,7 +26,10 @@
 //   10-13 gather producers: K rows 0-63, K rows 64-127, V rows 0-63, V rows 64-127 of
 //         every chunk, one warp per SM sub-partition, 16-byte cp.async into the
 //         128B-swizzled ring slots (3 K + 3 V)
-//   14, 15 idle
+//   14    tile scheduler: claims tiles from a global counter (atomicAdd, in the order of
+//         p.order when given: the host's per-head longest-first order) and hands them to every
+//         role through a 16-entry shared ring, so CTAs that draw short lists take more tiles
+//   15    idle
 // TMEM (512 cols): O [0, D) | Q [128, 128 + D/2) | S0 [256, 384) | S1 [384, 512).
 // P_j (bf16 pairs) overwrites S[j%2] cols 0..63.
 // Lazy rescale: the running max used for exp only moves when the row max grows
@@ -51,6 +54,9 @@ constexpr int NSOFT = 8;      // softmax warps
 constexpr int WARP_MMA0 = 8;  // MMA issuers 8 (buffer 0) and 9 (buffer 1)
 constexpr int WARP_PROD0 = 10;
 constexpr int NPROD = 4;      // gather producers 10-13
+constexpr int WARP_SCHED = 14;
+constexpr int NSCHED = 16;    // tile ring entries
+constexpr int NCONSUMERS = NSOFT + 2 + NPROD;  // warps that read every tile ring entry
 constexpr int NWARPS = 16;
 constexpr int REG_SOFTMAX = 184;
 constexpr int REG_OTHER = 72;  // producers and issuers: measured 13% slower at 64
@@ -81,9 +87,10 @@ struct WsSmem {
   static constexpr int OFF_K = 0;
   static constexpr int OFF_V = OFF_K + NSK * KV;
   static constexpr int OFF_BAR = OFF_V + NSV * KV;
-  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3 + 1;
+  static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3 + 1 + 2 * NSCHED;
   static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row
-  static constexpr int BYTES = OFF_XCH + 2 * 128 * 4;
+  static constexpr int OFF_SCHED = OFF_XCH + 2 * 128 * 4;                      // tile ring: int64 ids
+  static constexpr int BYTES = OFF_SCHED + NSCHED * 8;
   static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
   static_assert(WARP_PROD0 + NPROD <= NWARPS, "too many producer warps");
 };
@@ -100,6 +107,9 @@ struct Bars {
   uint64_t* q_full;     // count 8 (every softmax warp writes a part of Q)
   uint64_t* o_full;
   uint64_t* o_empty;    // count 8
+  uint64_t* sched_full;   // [NSCHED] count 1 (the scheduler's arrival after writing the entry)
+  uint64_t* sched_empty;  // [NSCHED] count NCONSUMERS
+  int64_t* sched_tile;    // [NSCHED] tile id, -1 = no more work
   uint32_t* tmem_slot;
 };
 
@@ -119,8 +129,56 @@ __device__ __forceinline__ Bars carve_bars(uint8_t* smem) {
   r.o_full = r.q_full + 1;
   r.o_empty = r.o_full + 1;
   r.pv_issued = r.o_empty + 1;
-  r.tmem_slot = reinterpret_cast<uint32_t*>(r.pv_issued + 1);
+  r.sched_full = r.pv_issued + 1;
+  r.sched_empty = r.sched_full + NSCHED;
+  r.tmem_slot = reinterpret_cast<uint32_t*>(r.sched_empty + NSCHED);
+  r.sched_tile = reinterpret_cast<int64_t*>(smem + L::OFF_SCHED);
   return r;
+}
+
+// ------------------------------------------------------------------ tile sequence
+// Every role walks the same tile sequence.  Static (p.sched == null): tile_begin + blockIdx.x,
+// strided by the grid.  Dynamic: the scheduler warp's ring; each consumer warp reads every entry
+// once, in order, and releases it.
+struct TileSeq {
+  uint32_t i = 0;
+  int64_t next_static;
+  __device__ explicit TileSeq(const AttnParams& p) : next_static(p.tile_begin + blockIdx.x) {}
+  __device__ __forceinline__ int64_t next(const AttnParams& p, const Bars& bar) {
+    if (p.sched == nullptr) {
+      const int64_t t = next_static;
+      next_static += gridDim.x;
+      return t < p.n_tiles ? t : -1;
+    }
+    const uint32_t slot = i % NSCHED;
+    mbar_wait(&bar.sched_full[slot], (i / NSCHED) & 1);
+    const int64_t t = *reinterpret_cast<volatile int64_t*>(&bar.sched_tile[slot]);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&bar.sched_empty[slot]);
+    ++i;
+    return t;
+  }
+};
+
+// Claims work items from p.sched until they run out; the CTA that draws the last of the
+// n_work + gridDim.x claims (every CTA makes exactly one failing claim) resets the counter to
+// zero for the next launch that uses this slot.
+__device__ __forceinline__ void tile_scheduler(const AttnParams& p, const Bars& bar) {
+  const uint32_t n_work = static_cast<uint32_t>(p.n_tiles - p.tile_begin);
+  for (uint32_t i = 0;; ++i) {
+    const uint32_t slot = i % NSCHED;
+    mbar_wait(&bar.sched_empty[slot], ((i / NSCHED) & 1) ^ 1);
+    const uint32_t w = atomicAdd(p.sched, 1u);
+    int64_t tile = -1;
+    if (w < n_work) {
+      tile = p.tile_begin + (p.order != nullptr ? __ldg(p.order + w) : static_cast<int64_t>(w));
+    } else if (w == n_work + gridDim.x - 1) {
+      atomicExch(p.sched, 0u);
+    }
+    *reinterpret_cast<volatile int64_t*>(&bar.sched_tile[slot]) = tile;
+    mbar_arrive(&bar.sched_full[slot]);
+    if (tile < 0) return;
+  }
 }
 
 // ------------------------------------------------------------------ producers
@@ -156,8 +214,10 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
   // the address is dstb[mm % PER] + compile-time immediate.
   constexpr int PER = 8 / RPI;
   uint32_t item = 0;
-  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+  TileSeq seq(p);
+  for (int64_t tile = seq.next(p, bar); tile >= 0; tile = seq.next(p, bar)) {
     const Tile t = decode_tile(p, tile);
+    if (kv == 0 && part == 0 && lane == 0) report_tile(p, t);
     const char* gsrc = static_cast<const char*>(kv ? p.v : p.k) + static_cast<int64_t>(t.row0) * (D * 2) + ch * 16;
     for (int c = 0; c < t.nchunks; ++c, ++item) {
       const uint32_t slot = item % nslot, use = item / nslot;
@@ -175,11 +235,10 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
         continue;
       }
       int keys[ROWS / 32];
+      bool oor = false;
 #pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) {
-        const int row = c * BN + part * ROWS + i * 32 + lane;
-        keys[i] = row < t.count ? __ldg(t.list + row) : -1;
-      }
+      for (int i = 0; i < ROWS / 32; ++i) keys[i] = load_key(p, t.list, c * BN + part * ROWS + i * 32 + lane, t.count, oor);
+      report_keys(p, oor);
       mbar_wait(&emptyb[slot], (use & 1) ^ 1);
       const char* src = gsrc;
       // opaque to the optimiser, so src + key * 2D stays one IMAD.WIDE.U32 per copy
@@ -234,7 +293,8 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
   const uint32_t tQ = tmem + TM_Q, tO = tmem + TM_O, tS = tmem + TM_S + r * 128;
   uint32_t c0 = 0;  // CTA-wide index of the tile's first chunk
   int it = 0;
-  for (int64_t tile = p.tile_begin + blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
+  TileSeq seq(p);
+  for (int64_t tile = seq.next(p, bar); tile >= 0; tile = seq.next(p, bar), ++it) {
     const Tile t = decode_tile(p, tile);
     mbar_wait(bar.q_full, it & 1);  // waited every tile, so the phase never runs two ahead
     if (r == 0) FGA_TT(p, it, 1);
@@ -371,8 +431,9 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
   uint32_t zero[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) zero[i] = 0u;
-  int64_t tile = p.tile_begin + blockIdx.x;
-  if (tile < p.n_tiles) {
+  TileSeq seq(p);
+  int64_t tile = seq.next(p, bar);
+  if (tile >= 0) {
     write_q<D>(p, qptr, decode_tile(p, tile), tmem, q, h, lane);
 #pragma unroll
     for (int i = 0; i < NQ32; ++i) tmem_st32(tOw + i * 32, zero);  // every PV accumulates into O
@@ -384,7 +445,7 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
       mbar_arrive(bar.o_empty);
     }
   }
-  for (; tile < p.n_tiles; tile += gridDim.x, ++it) {
+  for (int64_t next_tile; tile >= 0; tile = next_tile, ++it) {
     const Tile t = decode_tile(p, tile);
     float m_use[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};  // l_run: this thread's partial sums
     uint32_t sv[2][32];  // [column half][4k + 2*row + e]: rows r0/r0+8, col 64*half + 8k + 2a + e
@@ -494,8 +555,9 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
     }
     chunk += t.nchunks;
     // every S of this tile has been consumed, so Q may be replaced by the next tile's
-    if (tile + gridDim.x < p.n_tiles) {
-      write_q<D>(p, qptr, decode_tile(p, tile + gridDim.x), tmem, q, h, lane);
+    next_tile = seq.next(p, bar);
+    if (next_tile >= 0) {
+      write_q<D>(p, qptr, decode_tile(p, next_tile), tmem, q, h, lane);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -575,6 +637,10 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     mbar_init(bar.o_full, 2);
     mbar_init(bar.o_empty, NSOFT);
     mbar_init(bar.pv_issued, 1);
+    for (int i = 0; i < NSCHED; ++i) {
+      mbar_init(&bar.sched_full[i], 1);
+      mbar_init(&bar.sched_empty[i], NCONSUMERS);
+    }
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -602,6 +668,8 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
       mma_chain<D>(p, smem, bar, tmem, warp - WARP_MMA0);
     } else if (warp < WARP_PROD0 + NPROD) {
       producer_half<D>(p, &tmK2, &tmV2, smem, bar, (warp - WARP_PROD0) >> 1, (warp - WARP_PROD0) & 1, lane);
+    } else if (warp == WARP_SCHED && p.sched != nullptr && lane == 0) {
+      tile_scheduler(p, bar);
     }
   }
   tc_fence_before();
@@ -617,11 +685,9 @@ template <int D, bool F32>
 int launch_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, cudaStream_t stream) {
   auto kern = fga_attn_ws_kernel<D, F32>;
   const int smem = WsSmem<D>::BYTES;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return check_launch("cudaFuncSetAttribute(attn_ws)");
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const int rc = smem_opt_in(reinterpret_cast<const void*>(kern), smem, "attn_ws"); rc != FGA_OK)
+    return rc;
+  const int sms = sm_count();
   const int64_t span = p.n_tiles - p.tile_begin;
   const int64_t grid = span < sms ? span : sms;
   kern<<<static_cast<unsigned>(grid), 32 * NWARPS, smem, stream>>>(maps[3], maps[4], q, p);

@@ -1,7 +1,10 @@
 // C ABI of libfgattn.so (include/fgattn.h): argument validation, error
 // codes, TMA descriptor construction, and dispatch to the kernel launchers.
 #include <cstdio>
+#include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 
 #include "internal.h"
 
@@ -14,6 +17,10 @@ int launch_topk(const float* s, int64_t rows, int64_t n, int64_t k, uint8_t* kee
 int launch_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, uint8_t* keep, cudaStream_t st);
 int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, float* ws,
                             cudaStream_t st);
+int launch_validate(const int32_t* idx, int64_t stride, const int32_t* counts, int64_t rows, int64_t n,
+                    int32_t* status, cudaStream_t stream);
+int status_to_code(const int32_t* status, cudaStream_t stream, const char* what);
+int launch_tile_order(const int32_t* counts, const fga_shape& s, int32_t* order, cudaStream_t stream);
 
 namespace {
 thread_local std::string g_last_error;
@@ -44,6 +51,32 @@ int check_shape(const fga_shape& s) {
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+int smem_opt_in(const void* fn, int bytes, const char* what) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev, bytes})) return FGA_OK;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
+    return check_launch(what);
+  done.insert({fn, dev, bytes});
+  return FGA_OK;
+}
+
+int sm_count() {
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    cache[dev] = sms;
+  }
+  return cache[dev];
+}
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -78,7 +111,7 @@ using namespace fga;
 
 extern "C" {
 
-int fga_version(void) { return 100; }
+int fga_version(void) { return 200; }
 
 const char* fga_last_error(void) { return g_last_error.c_str(); }
 
@@ -116,27 +149,69 @@ int fga_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, i
                             static_cast<cudaStream_t>(stream));
 }
 
-int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
-                        const int32_t* counts, void* o, int o_dtype, float* lse, fga_shape shape, void* stream) {
+int fga_sparse_attn_fwd_ex(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
+                           const int32_t* counts, void* o, int o_dtype, float* lse, fga_shape shape, int64_t tile_begin,
+                           int64_t tile_end, const int32_t* order, int32_t* status, int flags, void* stream) {
   int rc = check_shape(shape);
   if (rc != FGA_OK) return rc;
   if (!q || !k || !v || !idx || !counts || !o) return fail(FGA_EINVAL, "null pointer");
   if (idx_group_stride < 1) return fail(FGA_EINVAL, "idx_group_stride must be >= 1");
   if (o_dtype != FGA_OUT_BF16 && o_dtype != FGA_OUT_F32) return fail(FGA_EINVAL, "o_dtype must be FGA_OUT_BF16 or FGA_OUT_F32");
-  return launch_attn(q, k, v, idx, idx_group_stride, counts, o, o_dtype, lse, shape, false,
-                     static_cast<cudaStream_t>(stream));
+  if ((flags & FGA_ATTN_CHECK) && status == nullptr) return fail(FGA_EINVAL, "FGA_ATTN_CHECK needs a status word");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (flags & FGA_ATTN_CHECK) {
+    if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess ||
+        cudaMemsetAsync(status + 1, 0x7f, sizeof(int32_t), st) != cudaSuccess)
+      return check_launch("fga_sparse_attn_fwd_ex (status reset)");
+  }
+  AttnLaunch a;
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.idx = idx;
+  a.idx_group_stride = idx_group_stride;
+  a.counts = counts;
+  a.o = o;
+  a.o_dtype = o_dtype;
+  a.lse = lse;
+  a.tile_begin = tile_begin;
+  a.tile_end = tile_end;
+  a.order = order;
+  a.status = status;
+  a.flags = flags;
+  rc = launch_attn(a, shape, st);
+  if (rc != FGA_OK || !(flags & FGA_ATTN_CHECK)) return rc;
+  return status_to_code(status, st, "fga_sparse_attn_fwd_ex");
+}
+
+int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
+                        const int32_t* counts, void* o, int o_dtype, float* lse, fga_shape shape, void* stream) {
+  return fga_sparse_attn_fwd_ex(q, k, v, idx, idx_group_stride, counts, o, o_dtype, lse, shape, 0, -1, nullptr,
+                                nullptr, 0, stream);
 }
 
 int fga_sparse_attn_fwd_tiles(const void* q, const void* k, const void* v, const int32_t* idx,
                               int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
                               fga_shape shape, int64_t tile_begin, int64_t tile_end, void* stream) {
+  return fga_sparse_attn_fwd_ex(q, k, v, idx, idx_group_stride, counts, o, o_dtype, lse, shape, tile_begin, tile_end,
+                                nullptr, nullptr, 0, stream);
+}
+
+int fga_validate_mask(const int32_t* idx, int64_t idx_group_stride, const int32_t* counts, int64_t rows, int64_t n,
+                      int32_t* status, void* stream) {
+  if (rows < 0 || n < 1 || idx_group_stride < 1) return fail(FGA_EINVAL, "rows >= 0, n >= 1 and stride >= 1 required");
+  if (!status || (rows > 0 && (!idx || !counts))) return fail(FGA_EINVAL, "null pointer");
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int rc = launch_validate(idx, idx_group_stride, counts, rows, n, status, st);
+  if (rc != FGA_OK) return rc;
+  return status_to_code(status, st, "fga_validate_mask");
+}
+
+int fga_tile_order(const int32_t* counts, fga_shape shape, int32_t* order, void* stream) {
   int rc = check_shape(shape);
   if (rc != FGA_OK) return rc;
-  if (!q || !k || !v || !idx || !counts || !o) return fail(FGA_EINVAL, "null pointer");
-  if (idx_group_stride < 1) return fail(FGA_EINVAL, "idx_group_stride must be >= 1");
-  if (o_dtype != FGA_OUT_BF16 && o_dtype != FGA_OUT_F32) return fail(FGA_EINVAL, "o_dtype must be FGA_OUT_BF16 or FGA_OUT_F32");
-  return launch_attn(q, k, v, idx, idx_group_stride, counts, o, o_dtype, lse, shape, false,
-                     static_cast<cudaStream_t>(stream), tile_begin, tile_end);
+  if (!counts || !order) return fail(FGA_EINVAL, "null pointer");
+  return launch_tile_order(counts, shape, order, static_cast<cudaStream_t>(stream));
 }
 
 int fga_dense_attn_fwd(const void* q, const void* k, const void* v, void* o, int o_dtype, float* lse,
@@ -145,7 +220,14 @@ int fga_dense_attn_fwd(const void* q, const void* k, const void* v, void* o, int
   if (rc != FGA_OK) return rc;
   if (!q || !k || !v || !o) return fail(FGA_EINVAL, "null pointer");
   if (o_dtype != FGA_OUT_BF16 && o_dtype != FGA_OUT_F32) return fail(FGA_EINVAL, "o_dtype must be FGA_OUT_BF16 or FGA_OUT_F32");
-  return launch_attn(q, k, v, nullptr, 0, nullptr, o, o_dtype, lse, shape, true, static_cast<cudaStream_t>(stream));
+  AttnLaunch a;
+  a.q = q;
+  a.k = k;
+  a.v = v;
+  a.o = o;
+  a.o_dtype = o_dtype;
+  a.lse = lse;
+  return launch_attn(a, shape, static_cast<cudaStream_t>(stream));
 }
 
 int fga_gather_rows(const void* matrix, int64_t rows, int64_t d, const int32_t* indices, int64_t n_idx, void* out,

@@ -57,8 +57,8 @@ template <int D>
 int launch_d(const CUtensorMap& tm, const int32_t* idx, int64_t n_idx, void* out, cudaStream_t st) {
   const int smem = (D / 64) * HALF + 64 + 1024;
   auto kern = fga_gather_kernel<D>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return check_launch("cudaFuncSetAttribute(gather)");
+  if (const int rc = smem_opt_in(reinterpret_cast<const void*>(kern), smem, "gather"); rc != FGA_OK)
+    return rc;
   const int64_t grid = (n_idx + CH - 1) / CH;
   kern<<<static_cast<unsigned>(grid), 32, smem, st>>>(tm, idx, n_idx, static_cast<uint16_t*>(out));
   return check_launch("fga_gather_kernel");

@@ -21,10 +21,31 @@ int check_launch(const char* what);
 int make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,
                       uint32_t box_rows);
 
-// Launchers (attn_sm100.cu / gather.cu / compact.cu / maskbuild.cu).
-int launch_attn(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
-                const int32_t* counts, void* o, int o_dtype, float* lse, const fga_shape& s, bool dense,
-                cudaStream_t stream, int64_t tile_begin = 0, int64_t tile_end = -1);
+// Opt `fn` into `bytes` of dynamic shared memory (once per kernel and device).
+int smem_opt_in(const void* fn, int bytes, const char* what);
+// Multiprocessor count of the current device (cached).
+int sm_count();
+
+// One attention launch (attn_launch.cu).  idx == nullptr means dense (contiguous key chunks).
+struct AttnLaunch {
+  const void* q = nullptr;
+  const void* k = nullptr;
+  const void* v = nullptr;
+  const int32_t* idx = nullptr;
+  int64_t idx_group_stride = 0;
+  const int32_t* counts = nullptr;
+  void* o = nullptr;
+  int o_dtype = FGA_OUT_BF16;
+  float* lse = nullptr;
+  int64_t tile_begin = 0;
+  int64_t tile_end = -1;
+  const int32_t* order = nullptr;
+  int32_t* status = nullptr;
+  int flags = 0;
+};
+
+// Launchers (attn_launch.cu / gather.cu / compact.cu / maskbuild.cu).
+int launch_attn(const AttnLaunch& a, const fga_shape& s, cudaStream_t stream);
 int launch_gather(const void* matrix, int64_t rows, int64_t d, const int32_t* indices, int64_t n_idx, void* out,
                   cudaStream_t stream);
 int launch_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bits, cudaStream_t stream);

@@ -410,11 +410,9 @@ template <int D, int PASS>
 int launch_pass(const CUtensorMap* maps, const CbParams& p, cudaStream_t st) {
   auto kern = cached_tc_kernel<D, PASS>;
   const int smem = CbSmem<D, PASS>::BYTES;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return check_launch("cudaFuncSetAttribute(cached_tc)");
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const int rc = smem_opt_in(reinterpret_cast<const void*>(kern), smem, "cached_tc"); rc != FGA_OK)
+    return rc;
+  const int sms = sm_count();
   const int64_t units = p.bh * p.tiles * (PASS == 2 ? p.kslabs : 1);
   kern<<<static_cast<unsigned>(units < sms ? units : sms), 32 * CB_WARPS, smem, st>>>(maps[0], maps[1], p);
   return check_launch("cached_tc_kernel");

@@ -127,6 +127,8 @@ def _parse_mask(buf: bytes):
     if words is None:
         raise CorruptionError("FGM1 payload is not a whole number of u32 words")
     rows = b * h * g
+    if b < 1 or h < 1 or rows > len(words):  # every row needs at least its length word
+        raise CorruptionError(f"FGM1 header dims (B={b}, H={h}, G={g}) overflow the {len(words)}-word payload")
     starts = np.empty(rows, np.int64)
     lens = np.empty(rows, np.int64)
     pos = 0
@@ -193,4 +195,5 @@ def read_mask_device(path_or_bytes, device=None, fill_sentinel: bool = False) ->
     counts = torch.empty((b, h, g), dtype=torch.int32, device=dev)
     _lib.call("fga_fgm1_unpack", payload.data_ptr(), starts_d.data_ptr(), b * h * g, n, idx.data_ptr(), n,
               counts.data_ptr(), 1 if fill_sentinel else 0, torch.cuda.current_stream(dev).cuda_stream)
-    return DeviceIndexMask(idx=idx, counts=counts, batch=b, heads=h, seq_len=n, group_size=m)
+    # _check_lists enforced the SparseIndexMask invariants on the host
+    return DeviceIndexMask(idx=idx, counts=counts, batch=b, heads=h, seq_len=n, group_size=m, validated=True)

@@ -74,8 +74,11 @@ def _round(cfg: AttnConfig) -> int:
     return 1 if cfg.precision == "bf16" else 0
 
 
-def _finish(keep, scores, cfg: AttnConfig, host: bool):
+def _finish(keep, scores, cfg: AttnConfig, host: bool, nonempty: bool = False):
+    """K1b compaction; with scores every list is non-empty (argmax fallback), and top-k keeps
+    k >= 1 keys, so those masks are valid by construction (no device check before first use)."""
     dm = compact_keep(keep, cfg.group_size, scores)
+    dm.validated = dm.validated or nonempty
     return dm.to_host() if host else dm
 
 
@@ -124,7 +127,7 @@ def build_mask_avg_query(q, k, cfg: AttnConfig, builder: MaskBuilderConfig, devi
         keep = t.empty(scores.shape, dtype=t.uint8, device=scores.device)
         rows = cfg.batch * cfg.heads * cfg.num_groups
         _lib.call("fga_topk_keep", ptr(scores), rows, cfg.seq_len, int(builder.top_k), ptr(keep), stream_ptr())
-        return _finish(keep, None, cfg, host)
+        return _finish(keep, None, cfg, host, nonempty=True)
     raise ValueError(f"strategy {builder.strategy!r} does not pool queries")
 
 

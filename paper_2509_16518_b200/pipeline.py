@@ -72,11 +72,14 @@ class HostPipeline:
         self.bits = t.empty((bh, g, self.words), dtype=t.int32, **kw)
         self.idx = t.empty((bh, g, n), dtype=t.int32, **kw)
         self.counts = t.empty((bh, g), dtype=t.int32, **kw)
+        # mask violations seen by the kernels (FGA_STATUS_* bits), read back once per call
+        self.status = t.zeros(2, dtype=t.int32, **kw)
+        self.status_host = t.zeros(2, dtype=t.int32).pin_memory()
         self.s_h2d = t.cuda.Stream(self.dev)
         self.s_cmp = t.cuda.Stream(self.dev)
         self.s_d2h = t.cuda.Stream(self.dev)
 
-    def __call__(self, q, k, v, keep_bits, out):
+    def __call__(self, q, k, v, keep_bits, out, check: bool = True):
         t = torch()
         cfg = self.cfg
         bh, n, d, g = cfg.batch * cfg.heads, cfg.seq_len, cfg.head_dim, cfg.num_groups
@@ -86,6 +89,9 @@ class HostPipeline:
         start = caller.record_event()
         for s_ in (self.s_h2d, self.s_cmp, self.s_d2h):
             s_.wait_event(start)
+        with t.cuda.stream(self.s_cmp):
+            self.status.zero_()
+        st = ptr(self.status)
         last = None
         m = cfg.group_size
         tpg = -(-m // 128)  # work tiles per group
@@ -104,9 +110,9 @@ class HostPipeline:
                     self.s_cmp.wait_event(ev_in)
                     _lib.call("fga_compact_bits", ptr(self.bits[h0, g0]), g1 - g0, n, ptr(self.idx[h0, g0]), n,
                               ptr(self.counts[h0, g0]), 0, cs)
-                    _lib.call("fga_sparse_attn_fwd_tiles", ptr(self.q[h0]), ptr(self.k[h0]), ptr(self.v[h0]),
+                    _lib.call("fga_sparse_attn_fwd_ex", ptr(self.q[h0]), ptr(self.k[h0]), ptr(self.v[h0]),
                               ptr(self.idx[h0]), n, ptr(self.counts[h0]), ptr(self.o[h0]), _lib.FGA_OUT_BF16, None,
-                              sh, g0 * tpg, g1 * tpg, cs)
+                              sh, g0 * tpg, g1 * tpg, None, st, 0, cs)
                     ev_c = self.s_cmp.record_event()
                     self.s_d2h.wait_event(ev_c)
                     with t.cuda.stream(self.s_d2h):
@@ -122,17 +128,27 @@ class HostPipeline:
             sh = _lib.shape(1, h1 - h0, n, d, cfg.group_size, cfg.scale)
             cs = self.s_cmp.cuda_stream
             _lib.call("fga_compact_bits", ptr(self.bits[h0]), rows, n, ptr(self.idx[h0]), n, ptr(self.counts[h0]), 0, cs)
-            _lib.call("fga_sparse_attn_fwd", ptr(self.q[h0]), ptr(self.k[h0]), ptr(self.v[h0]), ptr(self.idx[h0]), n,
-                      ptr(self.counts[h0]), ptr(self.o[h0]), _lib.FGA_OUT_BF16, None, sh, cs)
+            _lib.call("fga_sparse_attn_fwd_ex", ptr(self.q[h0]), ptr(self.k[h0]), ptr(self.v[h0]), ptr(self.idx[h0]),
+                      n, ptr(self.counts[h0]), ptr(self.o[h0]), _lib.FGA_OUT_BF16, None, sh, 0, -1, None, st, 0, cs)
             ev_c = self.s_cmp.record_event()
             self.s_d2h.wait_event(ev_c)
             with t.cuda.stream(self.s_d2h):
                 ho[h0:h1].copy_(self.o[h0:h1], non_blocking=True)
                 last = self.s_d2h.record_event()
+        # the status word follows the last attention launch on s_cmp
+        done_cmp = self.s_cmp.record_event()
+        self.s_d2h.wait_event(done_cmp)
+        with t.cuda.stream(self.s_d2h):
+            self.status_host.copy_(self.status, non_blocking=True)
+            last = self.s_d2h.record_event()
         caller.wait_event(last)
-        # keep the host buffers alive until the copies complete (stream-ordered on `caller`)
-        for x in (q, k, v, keep_bits, out):
-            x.record_stream(caller) if x.is_cuda else None
+        if check:
+            # an empty slice-mask row has no softmax denominator: the reference raises
+            # (sparse.py:47-48 on the mask, tiled.py:75-76 in finalize); the kernels only flag it
+            last.synchronize()
+            bits = int(self.status_host[0])
+            if bits & _lib.FGA_STATUS_EMPTY:
+                raise ValueError("every group needs at least one key (an all-zero keep_bits row)")
         return out
 
 
@@ -140,9 +156,11 @@ _pipes: dict = {}
 
 
 def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: int = 5, tail: bool = True,
-                          tail_parts: int = 2):
-    """FG-Attn from pinned host buffers (see module doc).  Returns the pinned host output;
-    synchronise the current stream before reading it."""
+                          tail_parts: int = 2, check: bool = True):
+    """FG-Attn from pinned host buffers (see module doc).  Returns the pinned host output.
+    With ``check`` (default) the call waits for the step and raises ValueError when a slice-mask
+    row keeps no key (sparse.py:47-48); with ``check=False`` it returns at once and the caller
+    synchronises the current stream before reading the output."""
     t = torch()
     for x in (q, k, v):
         if tuple(x.shape) != cfg.dims:
@@ -157,4 +175,4 @@ def sparse_attention_host(q, k, v, keep_bits, cfg: AttnConfig, out=None, slabs: 
         _pipes[key] = HostPipeline(cfg, slabs, tail=tail, tail_parts=tail_parts)
     if out is None:
         out = t.empty(cfg.dims, dtype=t.bfloat16, pin_memory=True)
-    return _pipes[key](q, k, v, keep_bits, out)
+    return _pipes[key](q, k, v, keep_bits, out, check)

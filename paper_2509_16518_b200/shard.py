@@ -21,7 +21,7 @@ import numpy as np
 from . import _lib
 from ._device import ptr, stream_ptr, torch
 from .core import AttnConfig
-from .sparse import DeviceIndexMask
+from .sparse import DeviceIndexMask, _as_device_mask
 
 __all__ = ["tile_work", "partition_tiles", "head_blocks", "sparse_attention_shard", "gather_outputs"]
 
@@ -68,6 +68,7 @@ def sparse_attention_shard(qd, kd, vd, mask: DeviceIndexMask, cfg: AttnConfig, t
     """Run tiles [begin, end) of the full problem into ``out`` (full-size CUDA tensor)."""
     t = torch()
     b, e = tile_range
+    mask = _as_device_mask(mask, cfg, qd.device.index)
     _lib.call("fga_sparse_attn_fwd_tiles", ptr(qd), ptr(kd), ptr(vd), ptr(mask.idx), mask.stride, ptr(mask.counts),
               ptr(out), _lib.FGA_OUT_F32 if out.dtype == t.float32 else _lib.FGA_OUT_BF16, None,
               _lib.shape(*cfg.dims, cfg.group_size, cfg.scale), int(b), int(e), stream_ptr())

@@ -22,7 +22,8 @@ torch CUDA bf16 inputs give device outputs.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import os
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -63,14 +64,14 @@ class SparseIndexMask:
                     a.flags.writeable = False
                     flat.append(a)
         self._lists = tuple(flat)
-        self._device = None
+        self._device = {}
 
     @classmethod
     def _from_flat(cls, batch, heads, seq_len, group_size, flat):
         m = cls.__new__(cls)
         m.batch, m.heads, m.seq_len, m.group_size = batch, heads, seq_len, group_size
         m._lists = tuple(flat)
-        m._device = None
+        m._device = {}
         return m
 
     @property
@@ -95,15 +96,17 @@ class SparseIndexMask:
             raise ShapeError(f"mask built for {ours}, config is {theirs}")
 
     def to_device(self, device=None) -> "DeviceIndexMask":
-        """Upload once (cached): padded int32 rows, ascending prefix then -1."""
-        if self._device is None:
+        """Upload once per device (cached): padded int32 rows, ascending prefix then -1.
+        The lists were validated on construction, so the device mask is marked validated."""
+        dev = require_device(device)
+        if dev not in self._device:
             pad = _padded_host(self)
             t = torch()
-            dev = require_device(device)
             idx = t.from_numpy(pad).to(f"cuda:{dev}")
             cnt = t.from_numpy(self.counts().astype(np.int32)).to(f"cuda:{dev}")
-            self._device = DeviceIndexMask(self.batch, self.heads, self.seq_len, self.group_size, idx, cnt)
-        return self._device
+            self._device[dev] = DeviceIndexMask(self.batch, self.heads, self.seq_len, self.group_size, idx, cnt,
+                                                validated=True)
+        return self._device[dev]
 
     def __eq__(self, other):
         if not isinstance(other, SparseIndexMask):
@@ -131,14 +134,19 @@ def _padded_host(mask: SparseIndexMask) -> np.ndarray:
 
 # ---------------------------------------------------------------- device mask
 
-@dataclass
+@dataclass(eq=False)
 class DeviceIndexMask:
     """Device-resident index mask: ``idx[B,H,G,stride]`` int32 + ``counts[B,H,G]`` int32.
 
-    ``idx[b,h,g,:counts[b,h,g]]`` lists the kept keys of group g; entries
+    ``idx[b,h,g,:counts[b,h,g]]`` lists the kept keys of group g, ascending; entries
     beyond the count are ignored by the kernels (they hold -1 when produced
     with ``fill_sentinel``).  This is the paper's [B, H, N/M, N] array
-     and the output of K1b."""
+     and the output of K1b.
+
+    ``validated`` records that the SparseIndexMask invariants (sparse.py:36-52:
+    1 <= count, keys in [0, N), sorted and unique) hold; producers that guarantee
+    them set it, anything else is checked once on the device (``validate``)
+    before its first use.  Treat the tensors as immutable after that."""
 
     batch: int
     heads: int
@@ -146,6 +154,8 @@ class DeviceIndexMask:
     group_size: int
     idx: object
     counts: object
+    validated: bool = False
+    _order: object = field(default=None, repr=False)
 
     @property
     def num_groups(self) -> int:
@@ -169,20 +179,48 @@ class DeviceIndexMask:
         c = int(self.counts[b, h, g].item())
         return self.idx[b, h, g, :c].cpu().numpy().astype(np.int64)
 
-    def validate(self) -> "DeviceIndexMask":
-        """Raise like SparseIndexMask would (sparse.py:47-52) for empty groups or
-        out-of-range keys.  One device reduction + a host sync."""
+    def check_layout(self, device=None) -> None:
+        """The tensor contract of the kernels: int32, contiguous, [B,H,G,stride] / [B,H,G],
+        on ``device``.  ShapeError otherwise (no device work)."""
         t = torch()
-        if int(self.counts.min().item()) < 1:
-            raise ValueError("every group needs at least one key")
-        if int(self.counts.max().item()) > self.stride:
-            raise ShapeError("counts exceed the index row stride")
-        col = t.arange(self.stride, device=self.idx.device, dtype=t.int32)
-        live = col < self.counts[..., None]
-        vals = t.where(live, self.idx, t.zeros_like(self.idx))
-        if int(vals.min().item()) < 0 or int(vals.max().item()) >= self.seq_len:
-            raise ValueError(f"key index out of range [0, {self.seq_len})")
+        want = (self.batch, self.heads, self.num_groups)
+        for name, x in (("idx", self.idx), ("counts", self.counts)):
+            if not is_torch(x) or not x.is_cuda:
+                raise ShapeError(f"DeviceIndexMask.{name} must be a CUDA tensor")
+            if x.dtype != t.int32:
+                raise ShapeError(f"DeviceIndexMask.{name} must be int32, got {x.dtype}")
+            if not x.is_contiguous():
+                raise ShapeError(f"DeviceIndexMask.{name} must be contiguous")
+            if device is not None and x.device.index != device:
+                raise ShapeError(f"DeviceIndexMask.{name} is on cuda:{x.device.index}, the inputs on cuda:{device}")
+        if tuple(self.idx.shape[:3]) != want or self.idx.dim() != 4 or self.stride < 1:
+            raise ShapeError(f"idx must be [B, H, G, stride] with [B, H, G] = {want}, got {tuple(self.idx.shape)}")
+        if tuple(self.counts.shape) != want:
+            raise ShapeError(f"counts must be {want}, got {tuple(self.counts.shape)}")
+
+    def validate(self) -> "DeviceIndexMask":
+        """Raise like SparseIndexMask would (sparse.py:47-52): ValueError for an empty group,
+        a key outside [0, N) or a list that is not strictly ascending; ShapeError for a count
+        above the row stride.  One HBM pass (fga_validate_mask) and a stream sync."""
+        self.check_layout()
+        t = torch()
+        status = t.empty(2, dtype=t.int32, device=self.idx.device)
+        rc, msg = _lib.call_rc("fga_validate_mask", ptr(self.idx), self.stride, ptr(self.counts),
+                               self.batch * self.heads * self.num_groups, self.seq_len, ptr(status), stream_ptr())
+        _raise_mask_status(rc, msg, int(status[0].item()) if rc != _lib.FGA_OK else 0)
+        self.validated = True
         return self
+
+    def tile_order(self, cfg: AttnConfig):
+        """Longest-first claim order of the work tiles within each head (fga_tile_order), cached."""
+        if self._order is None:
+            t = torch()
+            n = cfg.batch * cfg.heads * cfg.num_groups * (-(-cfg.group_size // 128))
+            order = t.empty(n, dtype=t.int32, device=self.idx.device)
+            _lib.call("fga_tile_order", ptr(self.counts), _lib.shape(*cfg.dims, cfg.group_size, cfg.scale), ptr(order),
+                      stream_ptr())
+            self._order = order
+        return self._order
 
     def to_host(self) -> SparseIndexMask:
         idx = self.idx.cpu().numpy().reshape(-1, self.stride)
@@ -193,15 +231,35 @@ class DeviceIndexMask:
         return SparseIndexMask._from_flat(self.batch, self.heads, self.seq_len, self.group_size, flat)
 
 
-def _as_device_mask(mask, cfg: AttnConfig | None = None) -> DeviceIndexMask:
+def _raise_mask_status(rc: int, msg: str, bits: int) -> None:
+    """FGA_STATUS_* / return codes -> the reference's exceptions (sparse.py:47-52: ValueError)."""
+    if rc == _lib.FGA_OK:
+        return
+    if bits & _lib.FGA_STATUS_EMPTY:
+        raise ValueError("every group needs at least one key")
+    if bits & _lib.FGA_STATUS_STRIDE:
+        raise ShapeError("counts exceed the index row stride")
+    if bits & _lib.FGA_STATUS_RANGE:
+        raise ValueError(f"key index out of range ({msg})")
+    if bits & _lib.FGA_STATUS_ORDER:
+        raise ValueError(f"key lists must be sorted and unique ({msg})")
+    _lib.check(rc, "mask check")
+
+
+def _as_device_mask(mask, cfg: AttnConfig | None = None, device=None) -> DeviceIndexMask:
+    """Device layout of any accepted mask; DeviceIndexMasks are layout-checked, and validated on
+    the device once unless their producer guarantees the invariants."""
     if isinstance(mask, DeviceIndexMask):
+        mask.check_layout(device)
+        if not mask.validated:
+            mask.validate()
         return mask
     if isinstance(mask, SparseIndexMask):
-        return mask.to_device()
+        return mask.to_device(device)
     if hasattr(mask, "keys_for") and hasattr(mask, "group_size"):  # a reference sliceattn mask
         lists = [[[mask.keys_for(b, h, g) for g in range(mask.num_groups)] for h in range(mask.heads)]
                  for b in range(mask.batch)]
-        return SparseIndexMask(mask.batch, mask.heads, mask.seq_len, mask.group_size, lists).to_device()
+        return SparseIndexMask(mask.batch, mask.heads, mask.seq_len, mask.group_size, lists).to_device(device)
     raise TypeError(f"unsupported mask type {type(mask).__name__}")
 
 
@@ -229,7 +287,8 @@ def compact_keep(keep, group_size: int, scores=None, fill_sentinel: bool = False
     idx = t.empty((b, h, g, n), dtype=t.int32, device=keep.device)
     cnt = t.empty((b, h, g), dtype=t.int32, device=keep.device)
     _lib.call("fga_compact", ptr(keep), ptr(sc), b * h * g, n, ptr(idx), n, ptr(cnt), int(fill_sentinel), stream_ptr())
-    return DeviceIndexMask(b, h, n, group_size, idx, cnt)
+    # with scores an empty row keeps its argmax, so every list is non-empty, ascending, in range
+    return DeviceIndexMask(b, h, n, group_size, idx, cnt, validated=sc is not None)
 
 
 def compact_keep_bits(bits, group_size: int, seq_len: int, fill_sentinel: bool = False) -> DeviceIndexMask:
@@ -316,13 +375,41 @@ def _check_qkv(cfg: AttnConfig, *ts):
             raise ShapeError(f"tensor dims {dims} do not match config {cfg.dims}")
 
 
+_KERNEL_FLAGS = {"": 0, "dual": 0, "ws": _lib.FGA_ATTN_PER_TILE, "static": _lib.FGA_ATTN_STATIC,
+                 "ws-static": _lib.FGA_ATTN_PER_TILE | _lib.FGA_ATTN_STATIC}
+
+
+def attn_flags() -> int:
+    """Kernel-selection flags for A/B runs: FGA_ATTN_KERNEL = ws (per-tile kernel for every
+    shape), static (static tile stride), ws-static; default: dual kernel for 129..256-row
+    groups, dynamic longest-first tile scheduling."""
+    return _KERNEL_FLAGS[os.environ.get("FGA_ATTN_KERNEL", "")]
+
+
+def _check_precision(cfg: AttnConfig, *ts) -> None:
+    """The kernels compute on bf16 operands with fp32 accumulation.  That is the reference's
+    precision='bf16' (inputs rounded on ingest, core.py:188-193); bf16 CUDA tensors are already
+    there.  precision='full' on fp32 data asks for fp32 operands (1e-4 vs the dense
+    oracle), which this path does not provide, so it is refused instead of silently rounded."""
+    if cfg.precision == "bf16":
+        return
+    t = torch()
+    if all(is_torch(x) and x.dtype == t.bfloat16 for x in ts):
+        return
+    raise NotImplementedError(
+        "precision='full' needs fp32 operands; the B200 kernels compute with bf16 operands and fp32 "
+        "accumulation -- use AttnConfig(..., precision='bf16') or pass bf16 CUDA tensors")
+
+
 def _run_sparse(qd, kd, vd, dmask: DeviceIndexMask, cfg: AttnConfig, out_dtype, lse: bool):
     t = torch()
     o = t.empty(cfg.dims, dtype=out_dtype, device=qd.device)
     l = t.empty(cfg.dims[:3], dtype=t.float32, device=qd.device) if lse else None
-    _lib.call("fga_sparse_attn_fwd", ptr(qd), ptr(kd), ptr(vd), ptr(dmask.idx), dmask.stride, ptr(dmask.counts),
+    flags = attn_flags()
+    order = None if flags & _lib.FGA_ATTN_STATIC else dmask.tile_order(cfg)
+    _lib.call("fga_sparse_attn_fwd_ex", ptr(qd), ptr(kd), ptr(vd), ptr(dmask.idx), dmask.stride, ptr(dmask.counts),
               ptr(o), _lib.FGA_OUT_F32 if out_dtype == t.float32 else _lib.FGA_OUT_BF16, ptr(l),
-              _lib.shape(*cfg.dims, cfg.group_size, cfg.scale), stream_ptr())
+              _lib.shape(*cfg.dims, cfg.group_size, cfg.scale), 0, -1, ptr(order), None, flags, stream_ptr())
     return o, l
 
 
@@ -346,10 +433,11 @@ def sparse_attention(q, k, v, mask, cfg: AttnConfig, trace: list | None = None, 
     chunk = cfg.group_size if chunk_size is None else chunk_size
     if chunk < 1 or chunk > cfg.group_size:
         raise ValueError(f"chunk_size must be in [1, {cfg.group_size}]")
-    dmask = _as_device_mask(mask, cfg)
     t = torch()
     host = not is_torch(q)
+    _check_precision(cfg, q, k, v)
     qd, kd, vd = as_device_bf16(q), as_device_bf16(k), as_device_bf16(v)
+    dmask = _as_device_mask(mask, cfg, qd.device.index)
     dt = t.float32 if host else (out_dtype or t.bfloat16)
     o, l = _run_sparse(qd, kd, vd, dmask, cfg, dt, return_lse)
     if trace is not None:
@@ -409,7 +497,17 @@ def import_padded(padded, group_size: int):
         col = t.arange(n, device=p.device, dtype=t.int32)
         if bool((used != (col < cnt[..., None])).any().item()):
             raise ValueError("sentinel slots must trail the key indices")
-        return DeviceIndexMask(b, h, n, group_size, p, cnt).validate()
+        # the host path builds a SparseIndexMask, whose np.unique sorts and deduplicates every
+        # list (sparse.py:46); do the same on the device so both give the same mask
+        big = t.iinfo(t.int32).max
+        srt = t.where(used, p, t.full_like(p, big)).sort(dim=-1).values
+        dup = t.zeros_like(used)
+        dup[..., 1:] = srt[..., 1:] == srt[..., :-1]
+        srt = t.where(dup, t.full_like(srt, big), srt).sort(dim=-1).values
+        live = srt != big
+        cnt = live.sum(-1, dtype=t.int32)
+        srt = t.where(live, srt, t.full_like(srt, -1)).contiguous()
+        return DeviceIndexMask(b, h, n, group_size, srt, cnt).validate()
     arr = np.asarray(padded)
     if arr.ndim != 4:
         raise ShapeError(f"expected [B, H, G, N] array, got shape {arr.shape}")
@@ -464,7 +562,9 @@ def random_mask_device(cfg: AttnConfig, density: float, seed: int = 0, fill_sent
     rows = cfg.batch * cfg.heads * cfg.num_groups
     keep = t.empty((cfg.batch, cfg.heads, cfg.num_groups, cfg.seq_len), dtype=t.uint8, device=f"cuda:{dev}")
     _lib.call("fga_random_keep", rows, cfg.seq_len, count, int(seed) & 0xFFFFFFFFFFFFFFFF, ptr(keep), stream_ptr())
-    return compact_keep(keep, cfg.group_size, None, fill_sentinel)
+    mask = compact_keep(keep, cfg.group_size, None, fill_sentinel)
+    mask.validated = True  # exactly max(1, round(d*N)) distinct keys per row
+    return mask
 
 
 def mask_jaccard(a, b) -> float:

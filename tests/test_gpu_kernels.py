@@ -41,11 +41,27 @@ def padded_dev(lists, b, h, n, m):
     return torch.from_numpy(pad).cuda(), torch.from_numpy(counts).cuda()
 
 
+def tile_order(counts, b, h, n, d, m):
+    tiles = b * h * (-(-n // m)) * (-(-m // 128))
+    order = torch.empty(tiles, dtype=torch.int32, device="cuda")
+    _lib.call("fga_tile_order", ptr(counts), _lib.shape(b, h, n, d, m), ptr(order), stream())
+    return order
+
+
 def run_sparse(q, k, v, idx, counts, b, h, n, d, m, scale=None, out_f32=True, lse=False):
+    """fga_sparse_attn_fwd_ex with the FGA_ATTN_KERNEL selection (attn_kernel fixture); the
+    dynamic scheduler claims tiles in fga_tile_order's longest-first order, with the kernel's
+    status checks on (FGA_ATTN_CHECK)."""
+    from paper_2509_16518_b200.sparse import attn_flags
+
+    flags = attn_flags()
+    order = None if flags & _lib.FGA_ATTN_STATIC else tile_order(counts, b, h, n, d, m)
+    status = torch.empty(2, dtype=torch.int32, device="cuda")
     o = torch.empty((b, h, n, d), device="cuda", dtype=torch.float32 if out_f32 else torch.bfloat16)
     l = torch.empty((b, h, n), device="cuda", dtype=torch.float32) if lse else None
-    _lib.call("fga_sparse_attn_fwd", ptr(q), ptr(k), ptr(v), ptr(idx), idx.shape[-1], ptr(counts), ptr(o),
-              _lib.FGA_OUT_F32 if out_f32 else _lib.FGA_OUT_BF16, ptr(l), _lib.shape(b, h, n, d, m, scale), stream())
+    _lib.call("fga_sparse_attn_fwd_ex", ptr(q), ptr(k), ptr(v), ptr(idx), idx.shape[-1], ptr(counts), ptr(o),
+              _lib.FGA_OUT_F32 if out_f32 else _lib.FGA_OUT_BF16, ptr(l), _lib.shape(b, h, n, d, m, scale),
+              0, -1, ptr(order), ptr(status), flags | _lib.FGA_ATTN_CHECK, stream())
     torch.cuda.synchronize()
     return o, l
 
@@ -124,11 +140,11 @@ def test_compact_unaligned_rows_without_scores():
 ATTN_CASES = [c for c in GOLDEN_CASES if c != "avgq_topk_ties"]
 
 
-@pytest.fixture(params=["default", "ws", "pp", "sync"])
+@pytest.fixture(params=["default", "ws", "static", "ws-static"])
 def attn_kernel(request, monkeypatch):
-    """The default dispatch (attn_ws.cu; attn_dual.cu for groups of 129..256 rows) and the kernels
-    FGA_ATTN_KERNEL selects: ws (attn_ws.cu for every shape), pp (attn_pp.cu) and sync (the
-    round-1 synchronous 4-warp kernel in attn_sm100.cu, kept as the simple baseline)."""
+    """The default dispatch (attn_ws.cu with the dynamic longest-first tile scheduler;
+    attn_dual.cu for groups of 129..256 rows) and the FGA_ATTN_KERNEL selections: ws (attn_ws.cu
+    for every shape), static (static tile stride), ws-static."""
     if request.param == "default":
         monkeypatch.delenv("FGA_ATTN_KERNEL", raising=False)
     else:

@@ -74,6 +74,10 @@ def test_mask_errors():
     bad[52 + 4 * (first - 1):52 + 4 * first] = (9999).to_bytes(4, "little")   # index >= N
     with pytest.raises(fio.CorruptionError):
         fio.decode_mask(bytes(bad))
+    huge = bytearray(buf)
+    huge[8:16] = (1 << 40).to_bytes(8, "little")   # B = 2^40: rejected before any allocation
+    with pytest.raises(fio.CorruptionError):
+        fio.decode_mask(bytes(huge))
 
 
 def test_committed_fixture_decodes_to_reference_lists(golden):
