@@ -86,7 +86,9 @@ def test_c2_builder_mask_variable_lengths():
     cfg = fga.AttnConfig(1, 2, 32760, 128, precision="bf16")
     g = torch.Generator(device="cuda").manual_seed(7)
     q, k, v = (torch.randn(cfg.dims, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
-    k[:, :, ::3] *= 2.0   # spread the pooled scores so the threshold keeps varying counts
+    # per-group query scales spread the pooled scores, so the threshold keeps 10-50% of the keys
+    f = torch.tensor([0.2 + 3.8 * (gi % 7) / 6 for gi in range(cfg.num_groups)], device="cuda")
+    q = (q.float() * f.repeat_interleave(cfg.group_size)[: cfg.seq_len, None]).to(torch.bfloat16)
     mask = fga.build_mask(q, k, cfg, fga.MaskBuilderConfig("avg_query_threshold", tau=1.02 / cfg.head_dim),
                           device_result=True)
     counts = mask.counts.cpu().numpy()
