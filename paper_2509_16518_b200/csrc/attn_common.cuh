@@ -146,22 +146,22 @@ int launch_attn_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, 
                    cudaStream_t stream);
 int launch_attn_dual(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
 
-// Producer-side mask checks.  load_key returns list[row] for row < count, else -1 (zero-fill);
-// a listed key outside [0, N) is replaced by row 0 (never read out of bounds) and flagged, and
-// report_keys() ORs FGA_STATUS_RANGE into p.status once per warp; report_tile() adds a tile's
-// count violations.
+// Producer-side mask checks.  The producers load their keys before waiting for a free ring slot
+// (the load latency hides behind the wait) and check them only afterwards: check_key() clamps a
+// listed key outside [0, N) to row 0 (never read out of bounds) and flags it, returns -1 (the
+// zero-fill sentinel) past the list end; report_keys() ORs FGA_STATUS_RANGE into p.status once
+// per warp; report_tile() adds a tile's count violations.
 #ifndef FGA_NO_MASK_CHECKS
 #define FGA_NO_MASK_CHECKS 0  // A/B builds only: skip the key range checks
 #endif
-__device__ __forceinline__ int load_key(const AttnParams& p, const int32_t* list, int row, int count, bool& oor) {
-  if (row >= count) return -1;
-  if (FGA_NO_MASK_CHECKS) return __ldg(list + row);
-  const int key = __ldg(list + row);
-  if (static_cast<unsigned>(key) < static_cast<unsigned>(p.seq_len)) return key;
+__device__ __forceinline__ int check_key(const AttnParams& p, int key, bool listed, bool& oor) {
+  if (!listed) return -1;
+  if (FGA_NO_MASK_CHECKS || static_cast<unsigned>(key) < static_cast<unsigned>(p.seq_len)) return key;
   oor = true;
   return 0;
 }
 __device__ __forceinline__ void report_keys(const AttnParams& p, bool oor) {
+  if (FGA_NO_MASK_CHECKS > 1) return;  // A/B builds only
   if (__any_sync(0xffffffffu, oor) && p.status != nullptr && (threadIdx.x & 31) == 0)
     atomicOr(p.status, FGA_STATUS_RANGE);
 }

@@ -122,16 +122,20 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem
     for (int c = 0; c < t.nchunks; ++c, ++item) {
       const uint32_t slot = item % nslot, use = item / nslot;
       int keys[ROWS / 32];
-      bool oor = false;
 #pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) keys[i] = load_key(p, t.list, c * BN + part * ROWS + i * 32 + lane, t.count, oor);
-      report_keys(p, oor);
+      for (int i = 0; i < ROWS / 32; ++i) {
+        const int row = c * BN + part * ROWS + i * 32 + lane;
+        keys[i] = row < t.count ? __ldg(t.list + row) : -1;
+      }
       mbar_wait(&emptyb[slot], (use & 1) ^ 1);          // tile 0's reads of the slot done
       mbar_wait(&emptyb[nslot + slot], (use & 1) ^ 1);  // and tile 1's
       // this thread's copies into the slot's previous use completed before the slot filled (the
       // empty waits imply it); the wait states it for tools that track cp.async per thread
       // (compute-sanitizer racecheck), and is a no-op here
       if (use > 0) asm volatile("cp.async.wait_group %0;" ::"n"(NSK > NSV ? NSV - 1 : NSK - 1) : "memory");
+      bool oor = false;  // checked after the wait, when the key loads have landed
+#pragma unroll
+      for (int i = 0; i < ROWS / 32; ++i) keys[i] = check_key(p, keys[i], c * BN + part * ROWS + i * 32 + lane < t.count, oor);
       const char* src = gsrc;
       asm volatile("mov.b64 %0, %0;" : "+l"(src));
       uint32_t dstb[PER];
@@ -159,6 +163,7 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem
         }
       }
       cp_async_arrive_noinc(&fullb[slot]);
+      report_keys(p, oor);
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
   }

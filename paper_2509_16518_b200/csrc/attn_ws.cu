@@ -235,11 +235,15 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
         continue;
       }
       int keys[ROWS / 32];
-      bool oor = false;
 #pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) keys[i] = load_key(p, t.list, c * BN + part * ROWS + i * 32 + lane, t.count, oor);
-      report_keys(p, oor);
+      for (int i = 0; i < ROWS / 32; ++i) {
+        const int row = c * BN + part * ROWS + i * 32 + lane;
+        keys[i] = row < t.count ? __ldg(t.list + row) : -1;
+      }
       mbar_wait(&emptyb[slot], (use & 1) ^ 1);
+      bool oor = false;  // checked after the wait, when the key loads have landed
+#pragma unroll
+      for (int i = 0; i < ROWS / 32; ++i) keys[i] = check_key(p, keys[i], c * BN + part * ROWS + i * 32 + lane < t.count, oor);
       const char* src = gsrc;
       // opaque to the optimiser, so src + key * 2D stays one IMAD.WIDE.U32 per copy
       asm volatile("mov.b64 %0, %0;" : "+l"(src));
@@ -270,6 +274,7 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
         }
       }
       cp_async_arrive_noinc(full);
+      report_keys(p, oor);
     }
   }
 }

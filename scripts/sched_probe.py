@@ -11,10 +11,7 @@ sys.path.insert(0, ".")
 import paper_2509_16518_b200 as fga  # noqa: E402
 
 
-def timeit(fn, iters=15):
-    flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    for _ in range(3):
-        fn()
+def timeit(fn, flush, iters=5):
     ts = []
     for _ in range(iters):
         flush.zero_()
@@ -24,7 +21,7 @@ def timeit(fn, iters=15):
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
-    return sorted(ts)[len(ts) // 2]
+    return ts
 
 
 cfg = fga.AttnConfig(1, 12, 32760, 128, precision="bf16")
@@ -37,14 +34,19 @@ for tau in (1.02, 1.05):
     m = fga.build_mask(qq, k, cfg, fga.MaskBuilderConfig("avg_query_threshold", tau=tau / cfg.head_dim),
                        device_result=True)
     masks[f"avgq_thr{tau}"] = m
+flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
 for name, m in masks.items():
     c = m.counts.float()
     flops = fga.count_flops(cfg, m).flops_matmul
-    row = {}
-    for mode in ("", "static"):
-        os.environ["FGA_ATTN_KERNEL"] = mode
-        t = timeit(lambda: fga.sparse_attention(q, k, v, m, cfg))
-        row[mode or "dynamic"] = t
-    print(f"{name}: density {float(c.mean()) / cfg.seq_len:.3f} count cv {float(c.std() / c.mean()):.3f} "
-          f"dynamic {row['dynamic']:.3f} ms ({flops / row['dynamic'] / 1e9:.0f} TF/s) "
-          f"static {row['static']:.3f} ms ({flops / row['static'] / 1e9:.0f} TF/s)", flush=True)
+    row = {"dynamic": [], "static": []}
+    for rnd in range(6):   # interleaved rounds: power / clock drift hits both modes alike
+        for mode in (("dynamic", "static") if rnd % 2 == 0 else ("static", "dynamic")):
+            os.environ["FGA_ATTN_KERNEL"] = "" if mode == "dynamic" else "static"
+            fga.sparse_attention(q, k, v, m, cfg)
+            row[mode] += timeit(lambda: fga.sparse_attention(q, k, v, m, cfg), flush)
+    out = []
+    for mode, ts in row.items():
+        ts.sort()
+        out.append(f"{mode} median {ts[len(ts) // 2]:.3f} min {ts[0]:.3f} ms ({flops / ts[0] / 1e9:.0f} TF/s at min)")
+    print(f"{name}: density {float(c.mean()) / cfg.seq_len:.3f} count cv {float(c.std() / c.mean()):.3f}  "
+          + "  ".join(out), flush=True)
