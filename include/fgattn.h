@@ -107,9 +107,10 @@ int fga_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, i
  *   lse    : optional fp32 [B, H, N] natural-log softmax normaliser.
  * Supported: head_dim in {64, 128}; any group_size in [1, N].
  * Masks that break the invariants never make the kernels read out of bounds
- * (counts are clamped to [0, stride], out-of-range keys read row 0) but give
- * unspecified rows; fga_validate_mask or the FGA_ATTN_CHECK flag of
- * fga_sparse_attn_fwd_ex report them as the reference does (sparse.py:47-52).
+ * (counts are clamped to [0, stride], keys to min(unsigned key, N-1)) but give
+ * unspecified rows (a group with no key gets zeros); fga_validate_mask or the
+ * FGA_ATTN_CHECK flag of fga_sparse_attn_fwd_ex report them as the reference
+ * does (sparse.py:47-52).
  */
 int fga_sparse_attn_fwd(const void* q, const void* k, const void* v, const int32_t* idx,
                         int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
@@ -134,7 +135,8 @@ int fga_sparse_attn_fwd_tiles(const void* q, const void* k, const void* v, const
 #define FGA_STATUS_ORDER 8   /* list not strictly ascending (fga_validate_mask) */
 
 /* fga_sparse_attn_fwd_ex flags */
-#define FGA_ATTN_CHECK 1     /* reset *status, run, synchronise, return FGA_EINVAL / FGA_ERANGE on violations */
+#define FGA_ATTN_CHECK 1     /* validate counts + key ranges first (status reset), run, synchronise, return
+                                FGA_EINVAL / FGA_ERANGE on violations (fga_validate_mask without the order check) */
 #define FGA_ATTN_PER_TILE 2  /* per-tile kernel also for 129..256-row groups (no shared-gather dual kernel)  */
 #define FGA_ATTN_STATIC 4    /* static tile stride instead of the dynamic tile scheduler                     */
 
@@ -143,8 +145,10 @@ int fga_sparse_attn_fwd_tiles(const void* q, const void* k, const void* v, const
  *   order  : optional int32 [tile_end - tile_begin]: the k-th tile claimed is
  *            tile_begin + order[k] (a permutation; e.g. longest lists first
  *            within each head, see fga_tile_order).  NULL = ascending.
- *   status : optional int32[2] device word; the kernel ORs FGA_STATUS_* bits
- *            into status[0] (the caller zeroes it, unless FGA_ATTN_CHECK).
+ *   status : optional int32[2] device word; the kernel ORs the count bits
+ *            (FGA_STATUS_EMPTY / _STRIDE) of the tiles it runs into status[0]
+ *            (the caller zeroes it, unless FGA_ATTN_CHECK, which also checks
+ *            the key ranges before the launch).
  *   flags  : FGA_ATTN_* bits.
  */
 int fga_sparse_attn_fwd_ex(const void* q, const void* k, const void* v, const int32_t* idx,

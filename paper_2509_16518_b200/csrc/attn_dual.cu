@@ -133,9 +133,8 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem
       // empty waits imply it); the wait states it for tools that track cp.async per thread
       // (compute-sanitizer racecheck), and is a no-op here
       if (use > 0) asm volatile("cp.async.wait_group %0;" ::"n"(NSK > NSV ? NSV - 1 : NSK - 1) : "memory");
-      bool oor = false;  // checked after the wait, when the key loads have landed
 #pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) keys[i] = check_key(p, keys[i], c * BN + part * ROWS + i * 32 + lane < t.count, oor);
+      for (int i = 0; i < ROWS / 32; ++i) keys[i] = clamp_key(p, keys[i], c * BN + part * ROWS + i * 32 + lane < t.count);
       const char* src = gsrc;
       asm volatile("mov.b64 %0, %0;" : "+l"(src));
       uint32_t dstb[PER];
@@ -163,7 +162,6 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem
         }
       }
       cp_async_arrive_noinc(&fullb[slot]);
-      report_keys(p, oor);
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
   }

@@ -241,9 +241,8 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
         keys[i] = row < t.count ? __ldg(t.list + row) : -1;
       }
       mbar_wait(&emptyb[slot], (use & 1) ^ 1);
-      bool oor = false;  // checked after the wait, when the key loads have landed
 #pragma unroll
-      for (int i = 0; i < ROWS / 32; ++i) keys[i] = check_key(p, keys[i], c * BN + part * ROWS + i * 32 + lane < t.count, oor);
+      for (int i = 0; i < ROWS / 32; ++i) keys[i] = clamp_key(p, keys[i], c * BN + part * ROWS + i * 32 + lane < t.count);
       const char* src = gsrc;
       // opaque to the optimiser, so src + key * 2D stays one IMAD.WIDE.U32 per copy
       asm volatile("mov.b64 %0, %0;" : "+l"(src));
@@ -274,7 +273,6 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
         }
       }
       cp_async_arrive_noinc(full);
-      report_keys(p, oor);
     }
   }
 }

@@ -18,7 +18,7 @@ int launch_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, ui
 int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, float* ws,
                             cudaStream_t st);
 int launch_validate(const int32_t* idx, int64_t stride, const int32_t* counts, int64_t rows, int64_t n,
-                    int32_t* status, cudaStream_t stream);
+                    int check_order, int32_t* status, cudaStream_t stream);
 int status_to_code(const int32_t* status, cudaStream_t stream, const char* what);
 int launch_tile_order(const int32_t* counts, const fga_shape& s, int32_t* order, cudaStream_t stream);
 
@@ -160,9 +160,17 @@ int fga_sparse_attn_fwd_ex(const void* q, const void* k, const void* v, const in
   if ((flags & FGA_ATTN_CHECK) && status == nullptr) return fail(FGA_EINVAL, "FGA_ATTN_CHECK needs a status word");
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (flags & FGA_ATTN_CHECK) {
-    if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess ||
-        cudaMemsetAsync(status + 1, 0x7f, sizeof(int32_t), st) != cudaSuccess)
-      return check_launch("fga_sparse_attn_fwd_ex (status reset)");
+    // counts and key ranges of the launch's groups (the kernel consumes lists in any order)
+    const int64_t G = (shape.seq_len + shape.group_size - 1) / shape.group_size;
+    const int64_t tpg = (shape.group_size + 127) / 128;
+    const int64_t n_tiles = shape.batch * shape.heads * G * tpg;
+    const int64_t tb = tile_begin < 0 ? 0 : tile_begin, te = tile_end < 0 ? n_tiles : tile_end;
+    const int64_t g0 = tb / tpg, g1 = te > tb ? (te + tpg - 1) / tpg : g0;
+    if (g1 > g0 && g1 <= shape.batch * shape.heads * G) {
+      rc = launch_validate(idx + g0 * idx_group_stride, idx_group_stride, counts + g0, g1 - g0, shape.seq_len, 0,
+                           status, st);
+      if (rc != FGA_OK) return rc;
+    }
   }
   AttnLaunch a;
   a.q = q;
@@ -202,7 +210,7 @@ int fga_validate_mask(const int32_t* idx, int64_t idx_group_stride, const int32_
   if (rows < 0 || n < 1 || idx_group_stride < 1) return fail(FGA_EINVAL, "rows >= 0, n >= 1 and stride >= 1 required");
   if (!status || (rows > 0 && (!idx || !counts))) return fail(FGA_EINVAL, "null pointer");
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int rc = launch_validate(idx, idx_group_stride, counts, rows, n, status, st);
+  const int rc = launch_validate(idx, idx_group_stride, counts, rows, n, 1, status, st);
   if (rc != FGA_OK) return rc;
   return status_to_code(status, st, "fga_validate_mask");
 }

@@ -17,7 +17,7 @@ namespace {
 
 __global__ void __launch_bounds__(256) fga_validate_kernel(const int32_t* __restrict__ idx, int64_t stride,
                                                            const int32_t* __restrict__ counts, int64_t rows, int n,
-                                                           int32_t* status) {
+                                                           int check_order, int32_t* status) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) fga_validate_kernel(const int32_t* __rest
   for (int j = lane; j < live; j += 32) {
     const int key = __ldg(list + j);
     oor |= static_cast<unsigned>(key) >= static_cast<unsigned>(n);
-    if (j > 0) order |= __ldg(list + j - 1) >= key;
+    if (check_order && j > 0) order |= __ldg(list + j - 1) >= key;
   }
   if (__any_sync(0xffffffffu, oor)) bad |= FGA_STATUS_RANGE;
   if (__any_sync(0xffffffffu, order)) bad |= FGA_STATUS_ORDER;
@@ -107,14 +107,14 @@ int launch_tile_order(const int32_t* counts, const fga_shape& s, int32_t* order,
 }
 
 int launch_validate(const int32_t* idx, int64_t stride, const int32_t* counts, int64_t rows, int64_t n,
-                    int32_t* status, cudaStream_t stream) {
+                    int check_order, int32_t* status, cudaStream_t stream) {
   if (cudaMemsetAsync(status, 0, sizeof(int32_t), stream) != cudaSuccess ||
       cudaMemsetAsync(status + 1, 0x7f, sizeof(int32_t), stream) != cudaSuccess)
     return check_launch("fga_validate_mask (status reset)");
   if (rows > 0) {
     const int64_t blocks = (rows + 7) / 8;
     fga_validate_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(idx, stride, counts, rows,
-                                                                          static_cast<int>(n), status);
+                                                                          static_cast<int>(n), check_order, status);
     if (const int rc = check_launch("fga_validate_kernel"); rc != FGA_OK) return rc;
   }
   return FGA_OK;
