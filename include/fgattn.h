@@ -22,6 +22,7 @@
 #ifndef FGATTN_H_
 #define FGATTN_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -193,14 +194,61 @@ int fga_gather_rows(const void* matrix, int64_t rows, int64_t d, const int32_t* 
                     void* out, void* stream);
 
 /*
+ * Device workspace.  The library never allocates device memory: operations
+ * that need scratch space take (ws, ws_bytes), a caller-owned buffer of at
+ * least fga_workspace_bytes(op, shape, round_bf16) bytes, 256-byte aligned,
+ * used stream-ordered on `stream` (reusable once the stream passes the call).
+ * Returns the byte count (>= 0), or a negative FGA_* code for a bad shape/op.
+ */
+#define FGA_WS_POOLED_SCORES 1    /* fga_pooled_scores, fga_pooled_scores_bf16 */
+#define FGA_WS_CACHED_GROUP_MAX 2 /* fga_cached_group_max                      */
+#define FGA_WS_BUILD_AVGQ 3       /* fga_build_mask_avgq                       */
+#define FGA_WS_BUILD_CACHED 4     /* fga_build_mask_cached                     */
+int64_t fga_workspace_bytes(int op, fga_shape shape, int round_bf16);
+
+/*
  * Average-query pooled scores (K1a, avg-query builder).  Replaces
  * masks.py:108-118 (pooled_query_scores):
  *   scores[b,h,g,j] = exp((k_j . mean_{i in g} q_i) * scale) / D   (fp32),
  *   rounded to bf16 (RNE, widened) when round_bf16 != 0.
  *   scores : fp32 [B, H, G, N].
  */
-int fga_pooled_scores(const void* q, const void* k, fga_shape shape, int round_bf16, float* scores,
-                      void* stream);
+int fga_pooled_scores(const void* q, const void* k, fga_shape shape, int round_bf16, float* scores, void* ws,
+                      size_t ws_bytes, void* stream);
+
+/* The same scores as bf16 bits (round_bf16 = 1 semantics, half the bytes):
+ * the input of fga_select_compact.  scores : uint16 [B, H, G, N]. */
+int fga_pooled_scores_bf16(const void* q, const void* k, fga_shape shape, uint16_t* scores, void* ws,
+                           size_t ws_bytes, void* stream);
+
+/*
+ * Selection + compaction in one kernel for bf16 scores (K1a tail + K1b).
+ * Replaces masks.py:131-147 followed by masks.py:75-91 / sparse.py:45-55:
+ *   FGA_SELECT_THRESHOLD: keep s >= tau; an empty row keeps [argmax(s)];
+ *   FGA_SELECT_TOPK     : the top_k largest, ties toward the smaller index;
+ * lists ascending in idx[row * idx_stride ...], counts[row]; fill_sentinel
+ * writes -1 up to n.  scores : uint16 bf16 bits [rows, n], n <= FGA_SELECT_MAX_N.
+ */
+#define FGA_SELECT_THRESHOLD 0
+#define FGA_SELECT_TOPK 1
+#define FGA_SELECT_MAX_N 114688
+int fga_select_compact(const uint16_t* scores, int64_t rows, int64_t n, int mode, float tau, int64_t top_k,
+                       int32_t* idx, int64_t idx_stride, int32_t* counts, int fill_sentinel, void* stream);
+
+/*
+ * Single-call mask builders (K1a -> K1b), lists straight into the device
+ * index layout.  fga_build_mask_avgq replaces masks.py:121-150
+ * (build_mask_avg_query; strategy FGA_SELECT_THRESHOLD with tau > 0, or
+ * FGA_SELECT_TOPK with 1 <= top_k <= N); fga_build_mask_cached replaces
+ * masks.py:94-105 on attention_map(q, k) (oracle.py:45-52) without the N x N
+ * map.  idx : int32 [B*H*G, idx_stride >= N]; counts : int32 [B*H*G].
+ */
+int fga_build_mask_avgq(const void* q, const void* k, fga_shape shape, int strategy, float tau, int64_t top_k,
+                        int round_bf16, int32_t* idx, int64_t idx_stride, int32_t* counts, int fill_sentinel,
+                        void* ws, size_t ws_bytes, void* stream);
+int fga_build_mask_cached(const void* q, const void* k, fga_shape shape, float tau, int round_bf16, int32_t* idx,
+                          int64_t idx_stride, int32_t* counts, int fill_sentinel, void* ws, size_t ws_bytes,
+                          void* stream);
 
 /* keep[i] = scores[i] >= tau  (masks.py:132 / masks.py:104). */
 int fga_threshold_keep(const float* scores, int64_t n_elems, float tau, uint8_t* keep, void* stream);
@@ -229,11 +277,10 @@ int fga_group_max_map(const float* map, int64_t bh, int64_t n, int64_t group_siz
  * oracle.py:45-52 (attention_map) + masks.py:66-72 (_group_max) as used by
  * masks.py:94-105 (build_mask_cached).
  *   gmax   : fp32 [B, H, G, N]; bf16-rounded when round_bf16 != 0.
- *   row_ws : fp32 workspace of at least B*H*N floats (row maxima); the fp64
- *            row denominators use a stream-ordered temporary allocation.
+ *   ws     : fga_workspace_bytes(FGA_WS_CACHED_GROUP_MAX, ...) bytes.
  */
-int fga_cached_group_max(const void* q, const void* k, fga_shape shape, int round_bf16, float* gmax,
-                         float* row_ws, void* stream);
+int fga_cached_group_max(const void* q, const void* k, fga_shape shape, int round_bf16, float* gmax, void* ws,
+                         size_t ws_bytes, void* stream);
 
 /*
  * Benchmark masks: every row keeps exactly `count` distinct keys chosen

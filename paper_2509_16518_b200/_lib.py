@@ -19,6 +19,9 @@ FGA_OK, FGA_EINVAL, FGA_ERANGE, FGA_ECUDA, FGA_EUNSUPPORTED = 0, -1, -2, -3, -4
 FGA_OUT_BF16, FGA_OUT_F32 = 0, 1
 FGA_STATUS_EMPTY, FGA_STATUS_RANGE, FGA_STATUS_STRIDE, FGA_STATUS_ORDER = 1, 2, 4, 8
 FGA_ATTN_CHECK, FGA_ATTN_PER_TILE, FGA_ATTN_STATIC = 1, 2, 4
+FGA_WS_POOLED_SCORES, FGA_WS_CACHED_GROUP_MAX, FGA_WS_BUILD_AVGQ, FGA_WS_BUILD_CACHED = 1, 2, 3, 4
+FGA_SELECT_THRESHOLD, FGA_SELECT_TOPK = 0, 1
+FGA_SELECT_MAX_N = 114688
 
 
 class FgaShape(ctypes.Structure):
@@ -30,6 +33,7 @@ _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I = ctypes.c_int
 _F = ctypes.c_float
+_SZ = ctypes.c_size_t
 
 _SIGS = {
     "fga_version": ([], _I),
@@ -46,11 +50,16 @@ _SIGS = {
     "fga_tile_order": ([_P, FgaShape, _P, _P], _I),
     "fga_dense_attn_fwd": ([_P, _P, _P, _P, _I, _P, FgaShape, _P], _I),
     "fga_gather_rows": ([_P, _I64, _I64, _P, _I64, _P, _P], _I),
-    "fga_pooled_scores": ([_P, _P, FgaShape, _I, _P, _P], _I),
+    "fga_workspace_bytes": ([_I, FgaShape, _I], _I64),
+    "fga_pooled_scores": ([_P, _P, FgaShape, _I, _P, _P, _SZ, _P], _I),
+    "fga_pooled_scores_bf16": ([_P, _P, FgaShape, _P, _P, _SZ, _P], _I),
+    "fga_select_compact": ([_P, _I64, _I64, _I, _F, _I64, _P, _I64, _P, _I, _P], _I),
+    "fga_build_mask_avgq": ([_P, _P, FgaShape, _I, _F, _I64, _I, _P, _I64, _P, _I, _P, _SZ, _P], _I),
+    "fga_build_mask_cached": ([_P, _P, FgaShape, _F, _I, _P, _I64, _P, _I, _P, _SZ, _P], _I),
     "fga_threshold_keep": ([_P, _I64, _F, _P, _P], _I),
     "fga_topk_keep": ([_P, _I64, _I64, _I64, _P, _P], _I),
     "fga_group_max_map": ([_P, _I64, _I64, _I64, _I, _P, _P], _I),
-    "fga_cached_group_max": ([_P, _P, FgaShape, _I, _P, _P, _P], _I),
+    "fga_cached_group_max": ([_P, _P, FgaShape, _I, _P, _P, _SZ, _P], _I),
     "fga_random_keep": ([_I64, _I64, _I64, ctypes.c_uint64, _P, _P], _I),
 }
 EXPORTED = tuple(_SIGS)
@@ -97,6 +106,14 @@ def call_rc(name: str, *args) -> tuple[int, str]:
     """Raw return code and message, for callers that map codes themselves."""
     rc = getattr(load(), name)(*args)
     return rc, ("" if rc == FGA_OK else load().fga_last_error().decode(errors="replace"))
+
+
+def workspace_bytes(op: int, shp: FgaShape, round_bf16: int = 1) -> int:
+    """Device workspace an operation needs (the library never allocates)."""
+    n = load().fga_workspace_bytes(int(op), shp, int(round_bf16))
+    if n < 0:
+        check(int(n), "fga_workspace_bytes")
+    return int(n)
 
 
 def shape(batch, heads, seq_len, head_dim, group_size, scale=None) -> FgaShape:

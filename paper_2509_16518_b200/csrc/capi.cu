@@ -1,22 +1,17 @@
 // C ABI of libfgattn.so (include/fgattn.h): argument validation, error
 // codes, TMA descriptor construction, and dispatch to the kernel launchers.
 #include <cstdio>
+#include <map>
 #include <mutex>
-#include <set>
 #include <string>
-#include <tuple>
+#include <utility>
 
 #include "internal.h"
 
 namespace fga {
 
-int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, float* scores, cudaStream_t st);
-int launch_threshold(const float* s, int64_t n, float tau, uint8_t* keep, cudaStream_t st);
 int launch_group_max_map(const float* map, int64_t bh, int64_t n, int64_t m, int round, float* gmax, cudaStream_t st);
-int launch_topk(const float* s, int64_t rows, int64_t n, int64_t k, uint8_t* keep, cudaStream_t st);
 int launch_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, uint8_t* keep, cudaStream_t st);
-int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, float* ws,
-                            cudaStream_t st);
 int launch_validate(const int32_t* idx, int64_t stride, const int32_t* counts, int64_t rows, int64_t n,
                     int check_order, int32_t* status, cudaStream_t stream);
 int status_to_code(const int32_t* status, cudaStream_t stream, const char* what);
@@ -53,15 +48,18 @@ int check_shape(const fga_shape& s) {
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 int smem_opt_in(const void* fn, int bytes, const char* what) {
+  // the attribute only ever grows per (kernel, device), so a smaller launch never lowers it under
+  // a larger one that already passed this check
   static std::mutex mu;
-  static std::set<std::tuple<const void*, int, int>> done;
+  static std::map<std::pair<const void*, int>, int> granted;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count({fn, dev, bytes})) return FGA_OK;
+  int& have = granted[{fn, dev}];
+  if (bytes <= have) return FGA_OK;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
     return check_launch(what);
-  done.insert({fn, dev, bytes});
+  have = bytes;
   return FGA_OK;
 }
 
@@ -244,11 +242,119 @@ int fga_gather_rows(const void* matrix, int64_t rows, int64_t d, const int32_t* 
   return launch_gather(matrix, rows, d, indices, n_idx, out, static_cast<cudaStream_t>(stream));
 }
 
-int fga_pooled_scores(const void* q, const void* k, fga_shape shape, int round_bf16, float* scores, void* stream) {
+int64_t fga_workspace_bytes(int op, fga_shape shape, int round_bf16) {
+  if (const int rc = check_shape(shape); rc != FGA_OK) return rc;
+  const int64_t G = (shape.seq_len + shape.group_size - 1) / shape.group_size;
+  const int64_t cells = shape.batch * shape.heads * G * shape.seq_len;  // [B, H, G, N]
+  switch (op) {
+    case FGA_WS_POOLED_SCORES:
+      return static_cast<int64_t>(ws_pooled_bytes(shape));
+    case FGA_WS_CACHED_GROUP_MAX:
+      return static_cast<int64_t>(ws_cached_bytes(shape));
+    case FGA_WS_BUILD_AVGQ:
+      if (round_bf16 && shape.seq_len <= FGA_SELECT_MAX_N)
+        return static_cast<int64_t>(ws_pooled_bytes(shape) + Workspace::align(2 * cells));
+      return static_cast<int64_t>(ws_pooled_bytes(shape) + Workspace::align(4 * cells) + Workspace::align(cells));
+    case FGA_WS_BUILD_CACHED:
+      return static_cast<int64_t>(ws_cached_bytes(shape) + Workspace::align(4 * cells) + Workspace::align(cells));
+    default:
+      return fail(FGA_EINVAL, "fga_workspace_bytes: unknown op");
+  }
+}
+
+namespace {
+int check_ws(void* ws) {
+  if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return fail(FGA_EINVAL, "workspace must be 256-byte aligned");
+  return FGA_OK;
+}
+}  // namespace
+
+int fga_pooled_scores(const void* q, const void* k, fga_shape shape, int round_bf16, float* scores, void* ws,
+                      size_t ws_bytes, void* stream) {
   int rc = check_shape(shape);
   if (rc != FGA_OK) return rc;
   if (!q || !k || !scores) return fail(FGA_EINVAL, "null pointer");
-  return launch_pooled_scores(q, k, shape, round_bf16, scores, static_cast<cudaStream_t>(stream));
+  if ((rc = check_ws(ws)) != FGA_OK) return rc;
+  Workspace w(ws, ws_bytes);
+  return launch_pooled_scores(q, k, shape, round_bf16, scores, nullptr, w, static_cast<cudaStream_t>(stream));
+}
+
+int fga_pooled_scores_bf16(const void* q, const void* k, fga_shape shape, uint16_t* scores, void* ws,
+                           size_t ws_bytes, void* stream) {
+  int rc = check_shape(shape);
+  if (rc != FGA_OK) return rc;
+  if (!q || !k || !scores) return fail(FGA_EINVAL, "null pointer");
+  if ((rc = check_ws(ws)) != FGA_OK) return rc;
+  Workspace w(ws, ws_bytes);
+  return launch_pooled_scores(q, k, shape, 1, nullptr, scores, w, static_cast<cudaStream_t>(stream));
+}
+
+int fga_select_compact(const uint16_t* scores, int64_t rows, int64_t n, int mode, float tau, int64_t top_k,
+                       int32_t* idx, int64_t idx_stride, int32_t* counts, int fill_sentinel, void* stream) {
+  if (rows > 0 && (!scores || !idx || !counts)) return fail(FGA_EINVAL, "null pointer");
+  return launch_select_compact(scores, rows, n, mode, tau, top_k, idx, idx_stride, counts, fill_sentinel,
+                               static_cast<cudaStream_t>(stream));
+}
+
+int fga_build_mask_avgq(const void* q, const void* k, fga_shape shape, int strategy, float tau, int64_t top_k,
+                        int round_bf16, int32_t* idx, int64_t idx_stride, int32_t* counts, int fill_sentinel,
+                        void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_shape(shape);
+  if (rc != FGA_OK) return rc;
+  if (!q || !k || !idx || !counts) return fail(FGA_EINVAL, "null pointer");
+  if (strategy == FGA_SELECT_THRESHOLD && !(tau > 0.f)) return fail(FGA_EINVAL, "threshold strategies need tau > 0");
+  if (strategy == FGA_SELECT_TOPK && (top_k < 1 || top_k > shape.seq_len))
+    return fail(FGA_EINVAL, "top_k must be in [1, seq_len]");
+  if (strategy != FGA_SELECT_THRESHOLD && strategy != FGA_SELECT_TOPK) return fail(FGA_EINVAL, "unknown strategy");
+  if (idx_stride < shape.seq_len) return fail(FGA_EINVAL, "idx_stride must be >= seq_len");
+  if ((rc = check_ws(ws)) != FGA_OK) return rc;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t G = (shape.seq_len + shape.group_size - 1) / shape.group_size;
+  const int64_t rows = shape.batch * shape.heads * G, n = shape.seq_len;
+  Workspace w(ws, ws_bytes);
+  if (round_bf16 && n <= FGA_SELECT_MAX_N) {  // bf16 scores -> fused selection + compaction
+    Workspace pw = w;
+    pw.take<char>(static_cast<int64_t>(ws_pooled_bytes(shape)));
+    uint16_t* s16 = pw.take<uint16_t>(rows * n);
+    if (s16 == nullptr) return fail(FGA_EINVAL, "build_mask_avgq: workspace too small (fga_workspace_bytes)");
+    if ((rc = launch_pooled_scores(q, k, shape, 1, nullptr, s16, w, st)) != FGA_OK) return rc;
+    return launch_select_compact(s16, rows, n, strategy, tau, top_k, idx, idx_stride, counts, fill_sentinel, st);
+  }
+  Workspace pw = w;
+  pw.take<char>(static_cast<int64_t>(ws_pooled_bytes(shape)));
+  float* sc = pw.take<float>(rows * n);
+  uint8_t* keep = pw.take<uint8_t>(rows * n);
+  if (sc == nullptr || keep == nullptr) return fail(FGA_EINVAL, "build_mask_avgq: workspace too small (fga_workspace_bytes)");
+  if ((rc = launch_pooled_scores(q, k, shape, round_bf16, sc, nullptr, w, st)) != FGA_OK) return rc;
+  if (strategy == FGA_SELECT_THRESHOLD) {
+    if ((rc = launch_threshold(sc, rows * n, tau, keep, st)) != FGA_OK) return rc;
+    return launch_compact(keep, sc, rows, n, idx, idx_stride, counts, fill_sentinel, st);
+  }
+  if ((rc = launch_topk(sc, rows, n, top_k, keep, st)) != FGA_OK) return rc;
+  return launch_compact(keep, nullptr, rows, n, idx, idx_stride, counts, fill_sentinel, st);
+}
+
+int fga_build_mask_cached(const void* q, const void* k, fga_shape shape, float tau, int round_bf16, int32_t* idx,
+                          int64_t idx_stride, int32_t* counts, int fill_sentinel, void* ws, size_t ws_bytes,
+                          void* stream) {
+  int rc = check_shape(shape);
+  if (rc != FGA_OK) return rc;
+  if (!q || !k || !idx || !counts) return fail(FGA_EINVAL, "null pointer");
+  if (!(tau > 0.f)) return fail(FGA_EINVAL, "tau must be positive");
+  if (idx_stride < shape.seq_len) return fail(FGA_EINVAL, "idx_stride must be >= seq_len");
+  if ((rc = check_ws(ws)) != FGA_OK) return rc;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t G = (shape.seq_len + shape.group_size - 1) / shape.group_size;
+  const int64_t rows = shape.batch * shape.heads * G, n = shape.seq_len;
+  Workspace w(ws, ws_bytes);
+  Workspace pw = w;
+  pw.take<char>(static_cast<int64_t>(ws_cached_bytes(shape)));
+  float* gmax = pw.take<float>(rows * n);
+  uint8_t* keep = pw.take<uint8_t>(rows * n);
+  if (gmax == nullptr || keep == nullptr) return fail(FGA_EINVAL, "build_mask_cached: workspace too small (fga_workspace_bytes)");
+  if ((rc = launch_cached_group_max(q, k, shape, round_bf16, gmax, w, st)) != FGA_OK) return rc;
+  if ((rc = launch_threshold(gmax, rows * n, tau, keep, st)) != FGA_OK) return rc;
+  return launch_compact(keep, gmax, rows, n, idx, idx_stride, counts, fill_sentinel, st);
 }
 
 int fga_threshold_keep(const float* scores, int64_t n_elems, float tau, uint8_t* keep, void* stream) {
@@ -269,12 +375,14 @@ int fga_group_max_map(const float* map, int64_t bh, int64_t n, int64_t group_siz
   return launch_group_max_map(map, bh, n, group_size, round_bf16, gmax, static_cast<cudaStream_t>(stream));
 }
 
-int fga_cached_group_max(const void* q, const void* k, fga_shape shape, int round_bf16, float* gmax, float* row_ws,
-                         void* stream) {
+int fga_cached_group_max(const void* q, const void* k, fga_shape shape, int round_bf16, float* gmax, void* ws,
+                         size_t ws_bytes, void* stream) {
   int rc = check_shape(shape);
   if (rc != FGA_OK) return rc;
-  if (!q || !k || !gmax || !row_ws) return fail(FGA_EINVAL, "null pointer");
-  return launch_cached_group_max(q, k, shape, round_bf16, gmax, row_ws, static_cast<cudaStream_t>(stream));
+  if (!q || !k || !gmax) return fail(FGA_EINVAL, "null pointer");
+  if ((rc = check_ws(ws)) != FGA_OK) return rc;
+  Workspace w(ws, ws_bytes);
+  return launch_cached_group_max(q, k, shape, round_bf16, gmax, w, static_cast<cudaStream_t>(stream));
 }
 
 int fga_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, uint8_t* keep, void* stream) {

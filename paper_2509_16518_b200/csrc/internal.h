@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -44,6 +45,28 @@ struct AttnLaunch {
   int flags = 0;
 };
 
+// Caller-provided device workspace (the C ABI never allocates): take() carves 256-byte aligned
+// pieces and returns nullptr when the remaining bytes do not suffice.
+struct Workspace {
+  char* p = nullptr;
+  size_t left = 0;
+  Workspace() = default;
+  Workspace(void* base, size_t bytes) : p(static_cast<char*>(base)), left(base ? bytes : 0) {}
+  static constexpr size_t align(size_t b) { return (b + 255) & ~size_t(255); }
+  template <class T>
+  T* take(int64_t count) {
+    const size_t bytes = align(static_cast<size_t>(count) * sizeof(T));
+    if (p == nullptr || bytes > left) return nullptr;
+    T* r = reinterpret_cast<T*>(p);
+    p += bytes;
+    left -= bytes;
+    return r;
+  }
+};
+// Workspace bytes per operation (fga_workspace_bytes), for a checked shape.
+size_t ws_pooled_bytes(const fga_shape& s);
+size_t ws_cached_bytes(const fga_shape& s);
+
 // Launchers (attn_launch.cu / gather.cu / compact.cu / maskbuild.cu).
 int launch_attn(const AttnLaunch& a, const fga_shape& s, cudaStream_t stream);
 int launch_gather(const void* matrix, int64_t rows, int64_t d, const int32_t* indices, int64_t n_idx, void* out,
@@ -54,9 +77,17 @@ int launch_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* 
 int launch_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, int64_t n, int32_t* idx,
                        int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream);
 int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s, int round, float* gmax,
-                               float* row_max, cudaStream_t st);
-int launch_pooled_scores_tc(const float* qbar, const void* k, const fga_shape& s, int round, float* scores,
+                               float* row_max, float* row_rinv, cudaStream_t st);
+int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, const void* k, const fga_shape& s, int round,
+                            float* scores, uint16_t* scores16, cudaStream_t st);
+int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, float* scores,
+                         uint16_t* scores16, Workspace& ws, cudaStream_t st);
+int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, Workspace& ws,
                             cudaStream_t st);
+int launch_threshold(const float* s, int64_t n, float tau, uint8_t* keep, cudaStream_t st);
+int launch_topk(const float* s, int64_t rows, int64_t n, int64_t k, uint8_t* keep, cudaStream_t st);
+int launch_select_compact(const uint16_t* scores, int64_t rows, int64_t n, int mode, float tau, int64_t top_k,
+                          int32_t* idx, int64_t idx_stride, int32_t* counts, int fill, cudaStream_t st);
 int launch_compact(const uint8_t* keep, const float* scores, int64_t rows, int64_t n, int32_t* idx,
                    int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream);
 

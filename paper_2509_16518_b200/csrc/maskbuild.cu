@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace fga {
 namespace {
@@ -37,6 +38,38 @@ __global__ void pooled_mean_kernel(const __nv_bfloat16* __restrict__ q, float* _
     for (int i = lo; i < hi; ++i) acc = __fadd_rn(acc, ld_bf16(q + (bh * N + i) * D + d));
     qbar[bhg * D + d] = __fdiv_rn(acc, static_cast<float>(hi - lo));
   }
+}
+
+// Same sums (each column added row by row, in order) with the group's rows -- one contiguous
+// M x D bf16 block -- brought into shared memory by TMA bulk copies first: one CTA of D threads
+// per group, thread = column.  Used when the block is 16-byte aligned and fits in 64 KB.
+constexpr int PM_MAX_BYTES = 64 * 1024;
+__global__ void pooled_mean_bulk_kernel(const __nv_bfloat16* __restrict__ q, float* __restrict__ qbar, int N, int D,
+                                        int M, int G) {
+  extern __shared__ __align__(16) __nv_bfloat16 s_rows[];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t bhg = blockIdx.x;
+  const int g = static_cast<int>(bhg % G);
+  const int64_t bh = bhg / G;
+  const int lo = g * M, hi = min(lo + M, N);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = static_cast<uint32_t>(hi - lo) * D * 2;
+    mbar_expect_tx(&bar, bytes);
+    const char* src = reinterpret_cast<const char*>(q + (bh * N + lo) * D);
+    for (uint32_t off = 0; off < bytes; off += 32768u)
+      bulk_g2s(reinterpret_cast<char*>(s_rows) + off, src + off, min(32768u, bytes - off), &bar);
+  }
+  mbar_wait(&bar, 0);
+  const int d = threadIdx.x;
+  float acc = 0.f;
+#pragma unroll 8
+  for (int i = 0; i < hi - lo; ++i) acc = __fadd_rn(acc, __bfloat162float(s_rows[i * D + d]));
+  qbar[bhg * D + d] = __fdiv_rn(acc, static_cast<float>(hi - lo));
 }
 
 // 64x64 fp32 tile of A[rows, D] . B[cols, D]^T, 256 threads, 4x4 per thread.
@@ -81,7 +114,8 @@ __device__ __forceinline__ void dot_tile(LA la, LB lb, int D, float (&acc)[4][4]
 constexpr int PT = 128, PDK = 32, PPAD = 4;
 __global__ void __launch_bounds__(256) pooled_scores128_kernel(const float* __restrict__ qbar,
                                                                const __nv_bfloat16* __restrict__ k,
-                                                               float* __restrict__ scores, int N, int D, int G,
+                                                               float* __restrict__ scores,
+                                                               uint16_t* __restrict__ scores16, int N, int D, int G,
                                                                float scale, int round) {
   __shared__ __align__(16) float As[PDK][PT + PPAD];  // [d][g]
   __shared__ __align__(16) float Bs[PDK][PT + PPAD];  // [d][j]
@@ -127,6 +161,10 @@ __global__ void __launch_bounds__(256) pooled_scores128_kernel(const float* __re
       const int j = j0 + (c < 4 ? tx * 4 + c : 64 + tx * 4 + c - 4);
       if (j >= N) continue;
       float s = __fdiv_rn(expf(__fmul_rn(acc[r][c], scale)), dd);
+      if (scores16 != nullptr) {
+        scores16[(bh * G + g) * N + j] = __bfloat16_as_ushort(__float2bfloat16_rn(s));
+        continue;
+      }
       if (round) s = bf16_rne(s);
       scores[(bh * G + g) * N + j] = s;
     }
@@ -471,33 +509,51 @@ int grid1d(int64_t n) { const int64_t b = (n + 255) / 256; return static_cast<in
 
 }  // namespace
 
+size_t ws_pooled_bytes(const fga_shape& s) {
+  const int64_t G = (s.seq_len + s.group_size - 1) / s.group_size;
+  const int64_t qrows = s.batch * s.heads * G;
+  return Workspace::align(sizeof(float) * qrows * s.head_dim) + Workspace::align(sizeof(__nv_bfloat16) * 3 * qrows * s.head_dim);
+}
+
+size_t ws_cached_bytes(const fga_shape& s) {
+  const int64_t rows = s.batch * s.heads * s.seq_len;
+  return Workspace::align(sizeof(float) * rows) + Workspace::align(sizeof(double) * rows);
+}
+
 int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, float* scores,
-                         cudaStream_t st) {
+                         uint16_t* scores16, Workspace& ws, cudaStream_t st) {
   const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
   const int64_t G = (N + M - 1) / M;
   if (D % DK != 0) return fail(FGA_EUNSUPPORTED, "pooled_scores: head_dim must be a multiple of 32");
-  float* qbar = nullptr;
-  if (cudaMallocAsync(&qbar, sizeof(float) * B * H * G * D, st) != cudaSuccess) return check_launch("cudaMallocAsync");
-  pooled_mean_kernel<<<static_cast<unsigned>(B * H * G), 128, 0, st>>>(
-      static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N), static_cast<int>(D), static_cast<int>(M),
-      static_cast<int>(G));
+  float* qbar = ws.take<float>(B * H * G * D);
+  __nv_bfloat16* parts = ws.take<__nv_bfloat16>(3 * B * H * G * D);
+  if (qbar == nullptr || parts == nullptr) return fail(FGA_EINVAL, "pooled_scores: workspace too small (fga_workspace_bytes)");
+  const int64_t blk = M * D * 2;
+  if (D % 8 == 0 && D <= 1024 && blk <= PM_MAX_BYTES && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+    if (const int rc = smem_opt_in(reinterpret_cast<const void*>(pooled_mean_bulk_kernel), static_cast<int>(blk),
+                                   "pooled_mean_bulk");
+        rc != FGA_OK)
+      return rc;
+    pooled_mean_bulk_kernel<<<static_cast<unsigned>(B * H * G), static_cast<unsigned>(D), static_cast<size_t>(blk),
+                              st>>>(static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N),
+                                    static_cast<int>(D), static_cast<int>(M), static_cast<int>(G));
+  } else {
+    pooled_mean_kernel<<<static_cast<unsigned>(B * H * G), 128, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N), static_cast<int>(D), static_cast<int>(M),
+        static_cast<int>(G));
+  }
   const char* cc = std::getenv("FGA_POOLED_CC");  // 1: the CUDA-core tile kernel below
   if (cc == nullptr || cc[0] != '1') {
-    const int rc = launch_pooled_scores_tc(qbar, k, s, round, scores, st);
-    if (rc != FGA_EUNSUPPORTED) {
-      cudaFreeAsync(qbar, st);
-      return rc;
-    }
+    const int rc = launch_pooled_scores_tc(qbar, parts, k, s, round, scores, scores16, st);
+    if (rc != FGA_EUNSUPPORTED) return rc;
   }
   const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
   dim3 grid(static_cast<unsigned>((N + PT - 1) / PT), static_cast<unsigned>((G + PT - 1) / PT),
             static_cast<unsigned>(B * H));
-  pooled_scores128_kernel<<<grid, 256, 0, st>>>(qbar, static_cast<const __nv_bfloat16*>(k), scores,
+  pooled_scores128_kernel<<<grid, 256, 0, st>>>(qbar, static_cast<const __nv_bfloat16*>(k), scores, scores16,
                                                 static_cast<int>(N), static_cast<int>(D), static_cast<int>(G), scale,
                                                 round);
-  int rc = check_launch("pooled_scores128_kernel");
-  cudaFreeAsync(qbar, st);
-  return rc;
+  return check_launch("pooled_scores128_kernel");
 }
 
 int launch_group_max_map(const float* map, int64_t bh, int64_t n, int64_t m, int round, float* gmax,
@@ -530,24 +586,22 @@ int launch_random_keep(int64_t rows, int64_t n, int64_t count, uint64_t seed, ui
   return check_launch("topk_kernel(random)");
 }
 
-int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, float* ws,
+int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, Workspace& ws,
                             cudaStream_t st) {
   const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
   const int64_t G = (N + M - 1) / M;
+  float* row_max = ws.take<float>(B * H * N);
+  double* row_den = ws.take<double>(B * H * N);  // the tensor-core passes use its first B*H*N floats (1/den)
+  if (row_max == nullptr || row_den == nullptr) return fail(FGA_EINVAL, "cached_group_max: workspace too small (fga_workspace_bytes)");
   // tensor-core passes for M = 128, D in {64, 128} (maskbuild_tc.cu); FGA_CACHED_CC=1 forces this file's
   // CUDA-core passes (kept for other shapes and as a cross-check)
   const char* cc = std::getenv("FGA_CACHED_CC");
   if (cc == nullptr || cc[0] != '1') {
-    const int rc = launch_cached_group_max_tc(q, k, s, round, gmax, ws, st);
+    const int rc = launch_cached_group_max_tc(q, k, s, round, gmax, row_max, reinterpret_cast<float*>(row_den), st);
     if (rc != FGA_EUNSUPPORTED) return rc;
   }
   if (D % DK != 0) return fail(FGA_EUNSUPPORTED, "cached_group_max: head_dim must be a multiple of 32");
   const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
-  // workspace: row max (fp32) in the first B*H*N floats; the fp64 denominators need 8-byte slots,
-  // so they live in a temporary buffer.
-  float* row_max = ws;
-  double* row_den = nullptr;
-  if (cudaMallocAsync(&row_den, sizeof(double) * B * H * N, st) != cudaSuccess) return check_launch("cudaMallocAsync");
   const auto* qb = static_cast<const __nv_bfloat16*>(q);
   const auto* kb = static_cast<const __nv_bfloat16*>(k);
   dim3 g1(static_cast<unsigned>((N + TILE - 1) / TILE), static_cast<unsigned>(B * H));
@@ -556,9 +610,7 @@ int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, in
   dim3 g2(static_cast<unsigned>((N + TILE - 1) / TILE), static_cast<unsigned>(G), static_cast<unsigned>(B * H));
   group_max_kernel<<<g2, 256, 0, st>>>(qb, kb, static_cast<int>(N), static_cast<int>(D), static_cast<int>(M),
                                        static_cast<int>(G), scale, row_max, row_den, round, gmax);
-  int rc = check_launch("cached_group_max");
-  cudaFreeAsync(row_den, st);
-  return rc;
+  return check_launch("cached_group_max");
 }
 
 }  // namespace fga

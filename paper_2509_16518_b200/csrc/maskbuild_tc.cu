@@ -92,7 +92,8 @@ struct CbParams {
   int nch;      // key chunks per unit: ceil(n / 128)
   int groups;   // pass 2: G
   int64_t part_rows;  // pass 2: rows of one q̄ part (B*H*G)
-  float* scores;      // pass 2: [B*H*G*N]
+  float* scores;      // pass 2: [B*H*G*N] fp32, or
+  uint16_t* scores16; // pass 2: [B*H*G*N] bf16 bits (the builders' input; p.round must be 1)
   int kslabs;         // pass 2: key ranges per (b*h, group tile)
   float scale;
   int round;
@@ -267,14 +268,23 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
           const int j = c * BN + row;
           constexpr float inv_d = 1.0f / D;  // D is a power of two: x / D == x * (1/D) exactly
           if (j < p.n) {
-            float* dst = p.scores + (bh * p.groups + t * BM + w * 32) * static_cast<int64_t>(p.n) + j;
+            const int64_t off = (bh * p.groups + t * BM + w * 32) * static_cast<int64_t>(p.n) + j;
             const int kmax = min(32, p.groups - (t * BM + w * 32));
+            if (p.scores16 != nullptr) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              if (k < kmax) {
-                float sc = __fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), p.scale)), inv_d);
-                if (p.round) sc = __bfloat162float(__float2bfloat16_rn(sc));
-                dst[static_cast<int64_t>(k) * p.n] = sc;
+              for (int k = 0; k < 32; ++k)
+                if (k < kmax)
+                  p.scores16[off + static_cast<int64_t>(k) * p.n] = __bfloat16_as_ushort(
+                      __float2bfloat16_rn(__fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), p.scale)), inv_d)));
+            } else {
+              float* dst = p.scores + off;
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                if (k < kmax) {
+                  float sc = __fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), p.scale)), inv_d);
+                  if (p.round) sc = __bfloat162float(__float2bfloat16_rn(sc));
+                  dst[static_cast<int64_t>(k) * p.n] = sc;
+                }
               }
             }
           }
@@ -423,7 +433,7 @@ int launch_pass(const CUtensorMap* maps, const CbParams& p, cudaStream_t st) {
 // Tensor-core cached builder; returns FGA_EUNSUPPORTED (caller uses the CUDA-core kernel)
 // unless M == 128 and D is 64 or 128.
 int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s, int round, float* gmax,
-                               float* row_max, cudaStream_t st) {
+                               float* row_max, float* rinv, cudaStream_t st) {
   const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
   if (M != 128 || (D != 64 && D != 128)) return FGA_EUNSUPPORTED;
   const int64_t rows = B * H * N;
@@ -432,8 +442,6 @@ int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s,
   int rc;
   if ((rc = make_tmap_bf16_2d(&maps[0], q, rows, D, 64, BM)) != FGA_OK) return rc;
   if ((rc = make_tmap_bf16_2d(&maps[1], k, rows, D, 64, BN)) != FGA_OK) return rc;
-  float* rinv = nullptr;
-  if (cudaMallocAsync(&rinv, sizeof(float) * rows, st) != cudaSuccess) return check_launch("cudaMallocAsync");
   CbParams p{};
   p.bh = B * H;
   p.n = static_cast<int>(N);
@@ -446,7 +454,6 @@ int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s,
   p.gmax = gmax;
   rc = D == 64 ? launch_pass<64, 0>(maps, p, st) : launch_pass<128, 0>(maps, p, st);
   if (rc == FGA_OK) rc = D == 64 ? launch_pass<64, 1>(maps, p, st) : launch_pass<128, 1>(maps, p, st);
-  cudaFreeAsync(rinv, st);
   return rc;
 }
 
@@ -468,16 +475,13 @@ __global__ void split3_kernel(const float* __restrict__ x, __nv_bfloat16* __rest
 
 // Avg-query scores s[b,h,g,j] = exp(k_j . q̄_g * scale) / D on the tensor cores (pass 2);
 // FGA_EUNSUPPORTED unless D is 64 or 128.  qbar: fp32 [B*H*G, D] (pooled_mean_kernel).
-int launch_pooled_scores_tc(const float* qbar, const void* k, const fga_shape& s, int round, float* scores,
-                            cudaStream_t st) {
+int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, const void* k, const fga_shape& s, int round,
+                            float* scores, uint16_t* scores16, cudaStream_t st) {
   const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
   if (D != 64 && D != 128) return FGA_EUNSUPPORTED;
   const int64_t G = (N + M - 1) / M;
   const int64_t rows = B * H * N, qrows = B * H * G;
   if (rows >= (int64_t(1) << 31) || 3 * qrows >= (int64_t(1) << 31)) return FGA_EUNSUPPORTED;
-  __nv_bfloat16* parts = nullptr;
-  if (cudaMallocAsync(&parts, sizeof(__nv_bfloat16) * 3 * qrows * D, st) != cudaSuccess)
-    return check_launch("cudaMallocAsync");
   split3_kernel<<<static_cast<unsigned>(std::min<int64_t>((qrows * D + 255) / 256, 148 * 16)), 256, 0, st>>>(
       qbar, parts, qrows * D);
   int rc = check_launch("split3_kernel");
@@ -493,13 +497,13 @@ int launch_pooled_scores_tc(const float* qbar, const void* k, const fga_shape& s
     p.groups = static_cast<int>(G);
     p.part_rows = qrows;
     p.scores = scores;
+    p.scores16 = scores16;
     // enough (b*h, group tile, key range) units for every SM, each at least 8 key chunks
     p.kslabs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(p.nch / 8, (4 * 148 + p.bh * p.tiles - 1) / (p.bh * p.tiles))));
     p.scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
     p.round = round;
     rc = D == 64 ? launch_pass<64, 2>(maps, p, st) : launch_pass<128, 2>(maps, p, st);
   }
-  cudaFreeAsync(parts, st);
   return rc;
 }
 

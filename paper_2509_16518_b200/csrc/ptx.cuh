@@ -102,6 +102,14 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uin
       "l"(policy)
       : "memory");
 }
+// 1D bulk copy global -> shared (TMA, no tensor map), completion on an mbarrier's tx count.
+// bytes: a multiple of 16; src and dst 16-byte aligned.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 // 16-byte cp.async (LDGSTS) that zero-fills when src_bytes == 0.
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)

@@ -1,0 +1,319 @@
+// K1a tail + K1b in one kernel for bf16-valued selection scores: threshold or top-k
+// selection fused with the compaction into ascending key lists.
+//
+// Reference semantics (/root/reference/pkg/src/sliceattn/masks.py):
+//   threshold (masks.py:131-132 + 75-91): keep j iff s_j >= tau, an empty row falls back to
+//       [argmax(s)] (first maximum);
+//   top-k (masks.py:133-147): the top_k largest s_j, ties toward the smaller index
+//       (np.lexsort((arange(n), -s))[:top_k]); SparseIndexMask (sparse.py:45-55) stores every
+//       list ascending.
+// The scores are bf16 (the builders' analysis_scores rounding, precision='bf16'), so each row is
+// a row of 16-bit keys: 2 bytes per score instead of 4 read from HBM, and the whole row fits in
+// shared memory (n <= FGA_SELECT_MAX_N), where the top-k threshold is found by a bisection over
+// key values -- one contention-free counting pass per bit of the occupied key range, each a
+// packed bf16x2 compare over LDS.128 and a block sum -- instead of histogram atomics, which the
+// clustered scores of the builders serialise on a few bins (maskbuild.cu topk_kernel).
+//
+// One 512-thread CTA per (b,h,g) row:
+//   1. load: global bf16 -> SMEM (+ min / max of the order-preserving 16-bit keys),
+//   2. top-k: thr = the largest value v with #{s >= v} >= k (bisection over [min, max] keys),
+//   3. count: warp w owns a contiguous range of 32-key words and counts its kept keys
+//      (> thr, == thr) with ballots; one block scan gives every warp its output offset and the
+//      number of threshold ties before its range (ties are kept in index order until k),
+//   4. emit: each warp writes its kept positions in order (ballot ranks, coalesced stores).
+// Output bit-exact with the reference lists for the same bf16 scores.  HBM-bound: 2n bytes read
+// and 4*count (+ the -1 tail) written per row.
+#include <cuda_bf16.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace fga {
+namespace {
+
+constexpr int SEL_THREADS = 512;
+constexpr int SEL_WARPS = SEL_THREADS / 32;
+
+// bf16 bits -> order-preserving unsigned key (negative values reversed below the positives)
+__device__ __forceinline__ uint32_t okey2(uint32_t w) {  // two packed keys
+  return w ^ ((((w >> 15) & 0x00010001u) * 0x7FFFu) | 0x80008000u);
+}
+__device__ __forceinline__ uint32_t okey_bits(uint32_t k) {  // inverse of okey2 for one key
+  return (k & 0x8000u) ? (k & 0x7FFFu) : (~k & 0xFFFFu);
+}
+__device__ __forceinline__ float bf16_value(uint32_t b) { return __uint_as_float(b << 16); }
+
+// sum over the block of one int per thread; `red` holds two buffers of SEL_WARPS (the phase
+// alternates, so one barrier per call suffices)
+__device__ __forceinline__ int block_sum(int v, int* red, int& phase) {
+  v = __reduce_add_sync(0xffffffffu, v);
+  int* r = red + phase * SEL_WARPS;
+  if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int s = 0;
+#pragma unroll
+  for (int w = 0; w < SEL_WARPS; ++w) s += r[w];
+  phase ^= 1;
+  return s;
+}
+
+template <bool TOPK>
+__global__ void __launch_bounds__(SEL_THREADS, 2)
+    select_compact_kernel(const uint16_t* __restrict__ scores, int64_t n64, float tau, int64_t top_k,
+                          int32_t* __restrict__ idx, int64_t stride, int32_t* __restrict__ counts, int fill) {
+  extern __shared__ __align__(16) uint16_t s_key[];  // the row's bf16 bits, padded with -NaN to a multiple of 8
+  __shared__ int s_red[2 * SEL_WARPS];
+  __shared__ int s_cnt[2][SEL_WARPS];
+  __shared__ unsigned long long s_best[SEL_WARPS];
+  __shared__ __align__(8) uint64_t s_bar;
+  const int n = static_cast<int>(n64);
+  const int64_t row = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint16_t* src = scores + row * n64;
+  int32_t* out = idx + row * stride;
+  const int nv = (n + 7) / 8;  // 16-byte vectors of keys
+  uint4* sv = reinterpret_cast<uint4*>(s_key);
+
+  // ---- 1. load (+ range of the order-preserving keys for the bisection)
+  uint32_t kmin2 = 0xFFFFFFFFu, kmax2 = 0u;
+  if ((n & 7) == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
+    // the whole row in one TMA bulk transfer (a few 32 KB copies on one mbarrier): the row
+    // arrives at the SM's bulk-copy rate instead of one DRAM latency per strided LDG round
+    if (tid == 0) {
+      mbar_init(&s_bar, 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t bytes = static_cast<uint32_t>(nv) * 16u;
+      mbar_expect_tx(&s_bar, bytes);
+      for (uint32_t off = 0; off < bytes; off += 32768u)
+        bulk_g2s(s_key + off / 2, src + off / 2, min(32768u, bytes - off), &s_bar);
+    }
+    mbar_wait(&s_bar, 0);
+    if (TOPK) {
+      for (int i = tid; i < nv; i += SEL_THREADS) {
+        const uint4 x = sv[i];
+        const uint32_t a = okey2(x.x), b = okey2(x.y), c = okey2(x.z), d = okey2(x.w);
+        kmin2 = __vminu2(kmin2, __vminu2(__vminu2(a, b), __vminu2(c, d)));
+        kmax2 = __vmaxu2(kmax2, __vmaxu2(__vmaxu2(a, b), __vmaxu2(c, d)));
+      }
+    }
+  } else {
+    for (int i = tid; i < 8 * nv; i += SEL_THREADS) {
+      uint32_t b = 0xFFFFu;  // pad: -NaN, which no comparison counts or keeps
+      if (i < n) {
+        b = __ldg(src + i);
+        if (TOPK) {
+          const uint32_t kk = okey2(b) & 0xFFFFu;
+          kmin2 = __vminu2(kmin2, kk | 0xFFFF0000u);
+          kmax2 = __vmaxu2(kmax2, kk);
+        }
+      }
+      s_key[i] = static_cast<uint16_t>(b);
+    }
+  }
+
+  int phase = 0;
+  float thr = 0.f;  // top-k: the k-th largest value
+  int need = 0;
+  if (TOPK) {
+    // ---- 2. bisection over the order-preserving keys: thr = max { v : #{s >= value(v)} >= k },
+    //      #{s >= value(kmin)} = n >= k.  Each pass counts with HSET2.BF16 (a 0xFFFF mask per
+    //      half-word that holds) accumulated by a 16x2 add: 2 instructions per 2 scores.
+    uint32_t lo = min(kmin2 & 0xFFFFu, kmin2 >> 16), hi = max(kmax2 & 0xFFFFu, kmax2 >> 16);
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (lane == 0) { s_red[warp] = static_cast<int>(lo); s_red[SEL_WARPS + warp] = static_cast<int>(hi); }
+    __syncthreads();  // also publishes s_key
+    lo = 0xFFFFu; hi = 0u;
+#pragma unroll
+    for (int w = 0; w < SEL_WARPS; ++w) {
+      lo = min(lo, static_cast<uint32_t>(s_red[w]));
+      hi = max(hi, static_cast<uint32_t>(s_red[SEL_WARPS + w]));
+    }
+    __syncthreads();  // s_red is reused by block_sum
+    const int k = static_cast<int>(top_k);
+    while (lo < hi) {  // block-uniform
+      const uint32_t mid = (lo + hi + 1) >> 1, pb = okey_bits(mid) * 0x00010001u;
+      const __nv_bfloat162 piv = *reinterpret_cast<const __nv_bfloat162*>(&pb);
+      uint32_t acc = 0;  // two 16-bit counters of -1s (|count| <= n/16 per thread each)
+      for (int i = tid; i < nv; i += SEL_THREADS) {
+        const uint4 x = sv[i];
+        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.x), piv));
+        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.y), piv));
+        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.z), piv));
+        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.w), piv));
+      }
+      const int mine = static_cast<int>(((0x10000u - (acc & 0xFFFFu)) & 0xFFFFu) + ((0x10000u - (acc >> 16)) & 0xFFFFu));
+      const int c = block_sum(mine, s_red, phase);
+      if (c >= k) lo = mid; else hi = mid - 1;
+    }
+    thr = bf16_value(okey_bits(lo));
+    need = k;  // minus the keys above thr: the ties at thr kept in index order
+  } else {
+    __syncthreads();
+  }
+
+  // ---- 3. per-warp counts over contiguous ranges of 256-key blocks (lane l: keys 8l..8l+7)
+  //      top-k: keys above thr and ties at thr; threshold: keys >= tau (a bf16 compare against
+  //      tau rounded up to bf16 is exact).  Masks accumulated 16x2 as in the bisection.
+  const uint32_t cut = TOPK ? __bfloat16_as_ushort(__float2bfloat16_rn(thr))
+                            : __bfloat16_as_ushort(__float2bfloat16_ru(tau));
+  const uint32_t cut2b = cut * 0x00010001u;
+  const __nv_bfloat162 cut2 = *reinterpret_cast<const __nv_bfloat162*>(&cut2b);
+  const int nb = (nv + 31) / 32;
+  const int bpw = (nb + SEL_WARPS - 1) / SEL_WARPS;
+  const int b0 = min(nb, warp * bpw), b1 = min(nb, b0 + bpw);
+  {
+    uint32_t ga = 0, ea = 0;
+    for (int b = b0; b < b1; ++b) {
+      const int vi = b * 32 + lane;
+      if (vi < nv) {
+        const uint4 x = sv[vi];
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
+          if (TOPK) {
+            ga = __vadd2(ga, __hgt2_mask(h, cut2));
+            ea = __vadd2(ea, __heq2_mask(h, cut2));
+          } else {
+            ga = __vadd2(ga, __hge2_mask(h, cut2));
+          }
+        }
+      }
+    }
+    const int g = static_cast<int>(((0x10000u - (ga & 0xFFFFu)) & 0xFFFFu) + ((0x10000u - (ga >> 16)) & 0xFFFFu));
+    const int e = static_cast<int>(((0x10000u - (ea & 0xFFFFu)) & 0xFFFFu) + ((0x10000u - (ea >> 16)) & 0xFFFFu));
+    const int gs = __reduce_add_sync(0xffffffffu, g), es = __reduce_add_sync(0xffffffffu, e);
+    if (lane == 0) { s_cnt[0][warp] = gs; s_cnt[1][warp] = es; }
+  }
+  __syncthreads();
+  int total_gt = 0, base = 0, eqrun = 0;
+#pragma unroll
+  for (int w = 0; w < SEL_WARPS; ++w) total_gt += s_cnt[0][w];
+  if (TOPK) need -= total_gt;  // >= 1 by the choice of thr
+  int total = total_gt;
+  if (TOPK) {
+    int er = 0;
+#pragma unroll
+    for (int w = 0; w < SEL_WARPS; ++w) {
+      const int e = s_cnt[1][w];
+      const int kept_e = max(0, min(e, need - er));
+      if (w < warp) { base += s_cnt[0][w] + kept_e; eqrun += e; }
+      er += e;
+      total += kept_e;
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < SEL_WARPS; ++w) base += w < warp ? s_cnt[0][w] : 0;
+  }
+
+  // ---- 4. emit, ascending: per 256-key block one packed warp scan of (kept-above, ties) counts;
+  //      the ties kept before lane l are min(tie prefix, ties still needed), so a lane's kept keys
+  //      are its above-cut keys plus its lowest few ties, written at consecutive positions.
+  for (int b = b0; b < b1; ++b) {
+    const int vi = b * 32 + lane;
+    uint32_t gm = 0, em = 0;  // bit j: key 8*vi + j
+    if (vi < nv) {
+      const uint4 x = sv[vi];
+      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float v = bf16_value((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+        if (TOPK) {
+          gm |= static_cast<uint32_t>(v > thr) << j;
+          em |= static_cast<uint32_t>(v == thr) << j;
+        } else {
+          gm |= static_cast<uint32_t>(v >= tau) << j;
+        }
+      }
+    }
+    const int gc = __popc(gm), ec = __popc(em);
+    const int packed = gc | (ec << 16);  // block counts <= 256 per half
+    int incl = packed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const int ex = incl - packed;
+    const int gpre = ex & 0xFFFF, epre = ex >> 16;
+    uint32_t keep = gm;
+    int at = base + gpre;  // this lane's kept keys go to out[at ...), ascending
+    if (TOPK) {
+      const int room = max(0, need - eqrun);  // ties still to be kept at the block start
+      const int mine = max(0, min(epre + ec, room) - min(epre, room));
+      at += min(epre, room);
+      if (mine == ec) {
+        keep |= em;
+      } else {
+        uint32_t m = em;
+        for (int i = 0; i < mine; ++i) { keep |= m & (0u - m); m &= m - 1u; }
+      }
+      base += (tot & 0xFFFF) + min(tot >> 16, room);
+      eqrun += tot >> 16;
+    } else {
+      base += tot & 0xFFFF;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (keep & (1u << j)) out[at++] = vi * 8 + j;
+  }
+
+  if (!TOPK && total == 0) {
+    // argmax fallback (masks.py:86-87): the largest value, first index (np.argmax); a NaN-free row
+    // of bf16 values orders like its order-preserving keys
+    unsigned long long best = 0ull;
+    for (int i = tid; i < n; i += SEL_THREADS) {
+      const unsigned long long v = (static_cast<unsigned long long>(okey2(s_key[i]) & 0xFFFFu) << 32) |
+                                   (0xFFFFFFFFu - static_cast<uint32_t>(i));
+      best = v > best ? v : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long v = __shfl_xor_sync(0xffffffffu, best, o);
+      best = v > best ? v : best;
+    }
+    if (lane == 0) s_best[warp] = best;
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 0; w < SEL_WARPS; ++w) best = s_best[w] > best ? s_best[w] : best;
+      out[0] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(best & 0xFFFFFFFFull));
+    }
+    total = 1;
+  }
+  if (tid == 0) counts[row] = total;
+  if (fill)
+    for (int i = total + tid; i < n; i += SEL_THREADS) out[i] = -1;
+}
+
+}  // namespace
+
+int launch_select_compact(const uint16_t* scores, int64_t rows, int64_t n, int mode, float tau, int64_t top_k,
+                          int32_t* idx, int64_t idx_stride, int32_t* counts, int fill, cudaStream_t st) {
+  if (rows < 0 || n < 1 || idx_stride < n) return fail(FGA_EINVAL, "select_compact: need rows >= 0, n >= 1, idx_stride >= n");
+  if (n > FGA_SELECT_MAX_N) return fail(FGA_EUNSUPPORTED, "select_compact: n exceeds FGA_SELECT_MAX_N (shared-memory row)");
+  if (mode != FGA_SELECT_THRESHOLD && mode != FGA_SELECT_TOPK) return fail(FGA_EINVAL, "select_compact: bad mode");
+  if (mode == FGA_SELECT_TOPK && (top_k < 1 || top_k > n)) return fail(FGA_EINVAL, "top_k must be in [1, n]");
+  if (rows == 0) return FGA_OK;
+  if (rows >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "select_compact: too many rows");
+  const int smem = static_cast<int>(((n + 7) / 8) * 16);
+  int rc;
+  if (mode == FGA_SELECT_TOPK) {
+    if ((rc = smem_opt_in(reinterpret_cast<const void*>(select_compact_kernel<true>), smem, "select_compact")) != FGA_OK)
+      return rc;
+    select_compact_kernel<true><<<static_cast<unsigned>(rows), SEL_THREADS, smem, st>>>(scores, n, tau, top_k, idx,
+                                                                                         idx_stride, counts, fill);
+  } else {
+    if ((rc = smem_opt_in(reinterpret_cast<const void*>(select_compact_kernel<false>), smem, "select_compact")) != FGA_OK)
+      return rc;
+    select_compact_kernel<false><<<static_cast<unsigned>(rows), SEL_THREADS, smem, st>>>(scores, n, tau, top_k, idx,
+                                                                                          idx_stride, counts, fill);
+  }
+  return check_launch("select_compact_kernel");
+}
+
+}  // namespace fga

@@ -25,7 +25,7 @@ import numpy as np
 from . import _lib
 from ._device import as_device, as_device_bf16, is_torch, ptr, stream_ptr, torch
 from .core import AttnConfig, ShapeError
-from .sparse import compact_keep
+from .sparse import DeviceIndexMask, compact_keep
 
 __all__ = [
     "STRATEGIES", "MaskBuilderConfig", "CachedMaskState", "refresh_policy", "build_mask_cached",
@@ -93,6 +93,14 @@ def _shape(cfg: AttnConfig):
     return _lib.shape(*cfg.dims, cfg.group_size, cfg.scale)
 
 
+def _workspace(op: int, cfg: AttnConfig, device):
+    """Caller-owned device workspace for ``op`` (the C ABI never allocates): a uint8 tensor
+    from torch's caching allocator (512-byte aligned)."""
+    t = torch()
+    n = _lib.workspace_bytes(op, _shape(cfg), _round(cfg))
+    return t.empty(max(n, 1), dtype=t.uint8, device=device)
+
+
 def pooled_query_scores(q, k, cfg: AttnConfig):
     """exp((k_j . mean_{i in g} q_i) * scale) / D as fp32 [B, H, G, N] (fga_pooled_scores)."""
     _check_qk(cfg, q, k)
@@ -100,7 +108,9 @@ def pooled_query_scores(q, k, cfg: AttnConfig):
     host = not is_torch(q)
     qd, kd = as_device_bf16(q), as_device_bf16(k)
     s = t.empty((cfg.batch, cfg.heads, cfg.num_groups, cfg.seq_len), dtype=t.float32, device=qd.device)
-    _lib.call("fga_pooled_scores", ptr(qd), ptr(kd), _shape(cfg), _round(cfg), ptr(s), stream_ptr())
+    ws = _workspace(_lib.FGA_WS_POOLED_SCORES, cfg, qd.device)
+    _lib.call("fga_pooled_scores", ptr(qd), ptr(kd), _shape(cfg), _round(cfg), ptr(s), ptr(ws), ws.numel(),
+              stream_ptr())
     return s.cpu().numpy() if host else s
 
 
@@ -111,24 +121,38 @@ def _threshold(scores, tau: float):
     return keep
 
 
+def _lists(cfg: AttnConfig, device):
+    t = torch()
+    idx = t.empty((cfg.batch, cfg.heads, cfg.num_groups, cfg.seq_len), dtype=t.int32, device=device)
+    cnt = t.empty((cfg.batch, cfg.heads, cfg.num_groups), dtype=t.int32, device=device)
+    return idx, cnt
+
+
 def build_mask_avg_query(q, k, cfg: AttnConfig, builder: MaskBuilderConfig, device_result: bool = False):
     """Avg-query builder (masks.py:121-150): threshold keeps s >= tau (argmax
-    fallback); top-k keeps the top_k largest, ties toward the smaller index."""
+    fallback); top-k keeps the top_k largest, ties toward the smaller index.
+
+    One C call (fga_build_mask_avgq): pooled scores on the tensor cores written as bf16,
+    then selection fused with the compaction (fga_select_compact); the [B,H,G,N] scores
+    never exist in fp32 and no keep bytes are written.  Every list is non-empty, ascending
+    and in range by construction."""
     _check_qk(cfg, q, k)
-    host = not is_torch(q) and not device_result
-    qd, kd = as_device_bf16(q), as_device_bf16(k)
-    scores = pooled_query_scores(qd, kd, cfg)
     if builder.strategy == "avg_query_threshold":
-        return _finish(_threshold(scores, builder.tau), scores, cfg, host)
-    if builder.strategy == "avg_query_topk":
+        strategy = _lib.FGA_SELECT_THRESHOLD
+    elif builder.strategy == "avg_query_topk":
+        strategy = _lib.FGA_SELECT_TOPK
         if builder.top_k > cfg.seq_len:
             raise ValueError(f"top_k {builder.top_k} exceeds seq_len {cfg.seq_len}")
-        t = torch()
-        keep = t.empty(scores.shape, dtype=t.uint8, device=scores.device)
-        rows = cfg.batch * cfg.heads * cfg.num_groups
-        _lib.call("fga_topk_keep", ptr(scores), rows, cfg.seq_len, int(builder.top_k), ptr(keep), stream_ptr())
-        return _finish(keep, None, cfg, host, nonempty=True)
-    raise ValueError(f"strategy {builder.strategy!r} does not pool queries")
+    else:
+        raise ValueError(f"strategy {builder.strategy!r} does not pool queries")
+    host = not is_torch(q) and not device_result
+    qd, kd = as_device_bf16(q), as_device_bf16(k)
+    idx, cnt = _lists(cfg, qd.device)
+    ws = _workspace(_lib.FGA_WS_BUILD_AVGQ, cfg, qd.device)
+    _lib.call("fga_build_mask_avgq", ptr(qd), ptr(kd), _shape(cfg), strategy, float(builder.tau),
+              int(builder.top_k), _round(cfg), ptr(idx), cfg.seq_len, ptr(cnt), 0, ptr(ws), ws.numel(), stream_ptr())
+    dm = DeviceIndexMask(cfg.batch, cfg.heads, cfg.seq_len, cfg.group_size, idx, cnt, validated=True)
+    return dm.to_host() if host else dm
 
 
 def build_mask_cached(map_, cfg: AttnConfig, tau: float, device_result: bool = False):
@@ -155,19 +179,27 @@ def cached_group_max(q, k, cfg: AttnConfig):
     t = torch()
     qd, kd = as_device_bf16(q), as_device_bf16(k)
     gmax = t.empty((cfg.batch, cfg.heads, cfg.num_groups, cfg.seq_len), dtype=t.float32, device=qd.device)
-    ws = t.empty(2 * cfg.batch * cfg.heads * cfg.seq_len, dtype=t.float32, device=qd.device)
-    _lib.call("fga_cached_group_max", ptr(qd), ptr(kd), _shape(cfg), _round(cfg), ptr(gmax), ptr(ws), stream_ptr())
+    ws = _workspace(_lib.FGA_WS_CACHED_GROUP_MAX, cfg, qd.device)
+    _lib.call("fga_cached_group_max", ptr(qd), ptr(kd), _shape(cfg), _round(cfg), ptr(gmax), ptr(ws), ws.numel(),
+              stream_ptr())
     return gmax
 
 
 def build_mask_cached_qk(q, k, cfg: AttnConfig, tau: float, device_result: bool = False):
     """The cached-threshold mask of ``build_mask_cached(attention_map(q, k))``
-    without materialising the N x N map (B200 path for Wan-scale N)."""
+    without materialising the N x N map (B200 path for Wan-scale N): one C call,
+    fga_build_mask_cached."""
     if tau <= 0:
         raise ValueError("tau must be positive")
+    _check_qk(cfg, q, k)
     host = not is_torch(q) and not device_result
-    gmax = cached_group_max(q, k, cfg)
-    return _finish(_threshold(gmax, tau), gmax, cfg, host)
+    qd, kd = as_device_bf16(q), as_device_bf16(k)
+    idx, cnt = _lists(cfg, qd.device)
+    ws = _workspace(_lib.FGA_WS_BUILD_CACHED, cfg, qd.device)
+    _lib.call("fga_build_mask_cached", ptr(qd), ptr(kd), _shape(cfg), float(tau), _round(cfg), ptr(idx),
+              cfg.seq_len, ptr(cnt), 0, ptr(ws), ws.numel(), stream_ptr())
+    dm = DeviceIndexMask(cfg.batch, cfg.heads, cfg.seq_len, cfg.group_size, idx, cnt, validated=True)
+    return dm.to_host() if host else dm
 
 
 def build_mask(q, k, cfg: AttnConfig, builder: MaskBuilderConfig, device_result: bool = False):

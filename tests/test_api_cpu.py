@@ -23,7 +23,7 @@ from paper_2509_16518_b200 import _lib
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "fgattn.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(fga_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(fga_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_header_symbol():

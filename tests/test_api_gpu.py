@@ -98,9 +98,18 @@ def test_avg_query_builders_match_reference(golden):
         srow_ref = g["scores"].reshape(len(ref), -1)[r]
         srow_gpu = scores.reshape(len(ref), -1)[r]
         assert all(srow_ref[j] != srow_gpu[j] for j in flip)
-    top = fga.build_mask_avg_query(q, k, cfg, fga.MaskBuilderConfig("avg_query_topk", top_k=int(g["top_k"])))
+    top_k = int(g["top_k"])
+    top = fga.build_mask_avg_query(q, k, cfg, fga.MaskBuilderConfig("avg_query_topk", top_k=top_k))
     topref = g.lists("topk_padded")
-    assert sum(not np.array_equal(a, b) for a, b in zip(top._lists, topref)) <= 1
+    rows_gpu = scores.reshape(len(topref), -1)
+    rows_ref = g["scores"].reshape(len(topref), -1)
+    for r in range(len(topref)):
+        # bit-exact with the reference selection on the GPU's own scores (masks.py:144-145) ...
+        own = np.sort(np.lexsort((np.arange(rows_gpu.shape[1]), -rows_gpu[r]))[:top_k])
+        assert np.array_equal(top._lists[r], own), r
+        # ... so a row can differ from the reference only where a score rounded differently
+        if not np.array_equal(top._lists[r], topref[r]):
+            assert (rows_gpu[r] != rows_ref[r]).any(), r
     fb = fga.build_mask_avg_query(q, k, cfg, fga.MaskBuilderConfig("avg_query_threshold", tau=1e9))
     assert all(np.array_equal(a, b) for a, b in zip(fb._lists, g.lists("fallback_padded")))
 
@@ -114,7 +123,17 @@ def test_cached_builders_match_reference(golden):
     m2 = fga.build_mask_cached_qk(q, k, cfg, float(g["tau"]))       # fused, no N x N map
     ref = g.lists()
     assert all(np.array_equal(a, b) for a, b in zip(m1._lists, ref))
-    assert sum(not np.array_equal(a, b) for a, b in zip(m2._lists, ref)) <= 1
+    gmax_gpu = fga.cached_group_max(q, k, cfg).cpu().numpy().reshape(len(ref), -1)
+    gmax_ref = oracle.cached_keep(oracle.attention_map(g.q, g.k, None, "bf16"), g.group_size, float(g["tau"]),
+                                  "bf16")[1].reshape(len(ref), -1)
+    tau = np.float32(g["tau"])
+    for r in range(len(ref)):
+        # keys may only flip where the fused group max differs from the map's (a bf16 step)
+        flip = set(m2._lists[r].tolist()) ^ set(ref[r].tolist())
+        assert all(gmax_gpu[r, j] != gmax_ref[r, j] for j in flip), r
+        keep = np.flatnonzero(gmax_gpu[r] >= tau)
+        own = keep if keep.size else np.array([int(np.argmax(gmax_gpu[r]))])
+        assert np.array_equal(m2._lists[r], own), r  # bit-exact on its own statistics
     fb = fga.build_mask_cached(amap, cfg, 2.0)
     assert all(np.array_equal(a, b) for a, b in zip(fb._lists, g.lists("fallback_padded")))
     assert all(len(x) == 1 for x in fb._lists)

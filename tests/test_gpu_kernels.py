@@ -30,6 +30,10 @@ def stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+def workspace(op, shp):
+    return torch.empty(max(_lib.workspace_bytes(op, shp), 1), dtype=torch.uint8, device="cuda")
+
+
 def to_bf16_dev(x):
     return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda().to(torch.bfloat16)
 
@@ -328,7 +332,8 @@ def test_pooled_scores_and_threshold_keep(golden):
     q, k = (to_bf16_dev(oracle.bf16_round(t)) for t in (g.q, g.k))
     gcount = oracle.num_groups(n, m)
     s = torch.empty((b, h, gcount, n), device="cuda", dtype=torch.float32)
-    _lib.call("fga_pooled_scores", ptr(q), ptr(k), _lib.shape(b, h, n, d, m), 1, ptr(s), stream())
+    ws = workspace(_lib.FGA_WS_POOLED_SCORES, _lib.shape(b, h, n, d, m))
+    _lib.call("fga_pooled_scores", ptr(q), ptr(k), _lib.shape(b, h, n, d, m), 1, ptr(s), ptr(ws), ws.numel(), stream())
     keep = torch.empty((b, h, gcount, n), device="cuda", dtype=torch.uint8)
     tau = float(g["tau"])
     _lib.call("fga_threshold_keep", ptr(s), s.numel(), tau, ptr(keep), stream())
@@ -356,7 +361,9 @@ def test_pooled_scores_tensor_cores_vs_oracle(n, d, h, m, monkeypatch):
     for cc in ("0", "1"):
         monkeypatch.setenv("FGA_POOLED_CC", cc)
         s = torch.full((b, h, gc, n), -1.0, device="cuda", dtype=torch.float32)
-        _lib.call("fga_pooled_scores", ptr(qd), ptr(kd), _lib.shape(b, h, n, d, m), 1, ptr(s), stream())
+        ws = workspace(_lib.FGA_WS_POOLED_SCORES, _lib.shape(b, h, n, d, m))
+        _lib.call("fga_pooled_scores", ptr(qd), ptr(kd), _lib.shape(b, h, n, d, m), 1, ptr(s), ptr(ws), ws.numel(),
+                  stream())
         torch.cuda.synchronize()
         got = s.cpu().numpy()
         mism = got != ref
@@ -386,8 +393,9 @@ def test_cached_group_max(golden):
     q, k = (to_bf16_dev(oracle.bf16_round(t)) for t in (g.q, g.k))
     gc = oracle.num_groups(n, m)
     gmax = torch.empty((b, h, gc, n), device="cuda", dtype=torch.float32)
-    ws = torch.empty(2 * b * h * n, device="cuda", dtype=torch.float32)
-    _lib.call("fga_cached_group_max", ptr(q), ptr(k), _lib.shape(b, h, n, d, m), 1, ptr(gmax), ptr(ws), stream())
+    ws = workspace(_lib.FGA_WS_CACHED_GROUP_MAX, _lib.shape(b, h, n, d, m))
+    _lib.call("fga_cached_group_max", ptr(q), ptr(k), _lib.shape(b, h, n, d, m), 1, ptr(gmax), ptr(ws), ws.numel(),
+              stream())
     torch.cuda.synchronize()
     got = gmax.cpu().numpy()
     ref = g["gmax"]
@@ -413,8 +421,9 @@ def test_cached_group_max_tensor_cores_vs_oracle(n, d, h, monkeypatch):
     for cc in ("0", "1"):
         monkeypatch.setenv("FGA_CACHED_CC", cc)
         gmax = torch.full((b, h, gc, n), -1.0, device="cuda", dtype=torch.float32)
-        ws = torch.empty(2 * b * h * n, device="cuda", dtype=torch.float32)
-        _lib.call("fga_cached_group_max", ptr(qd), ptr(kd), _lib.shape(b, h, n, d, m), 1, ptr(gmax), ptr(ws), stream())
+        ws = workspace(_lib.FGA_WS_CACHED_GROUP_MAX, _lib.shape(b, h, n, d, m))
+        _lib.call("fga_cached_group_max", ptr(qd), ptr(kd), _lib.shape(b, h, n, d, m), 1, ptr(gmax), ptr(ws),
+                  ws.numel(), stream())
         torch.cuda.synchronize()
         got = gmax.cpu().numpy()
         mism = got != ref
@@ -451,9 +460,10 @@ def test_cached_group_max_tensor_cores_mismatch_rate_large(n, cc, monkeypatch):
     keep_ref, ref = oracle.cached_keep(amap, m, 0.5 / n, "bf16")
     gc = oracle.num_groups(n, m)
     gmax = torch.full((1, h, gc, n), -1.0, device="cuda", dtype=torch.float32)
-    ws = torch.empty(2 * h * n, device="cuda", dtype=torch.float32)
+    ws = workspace(_lib.FGA_WS_CACHED_GROUP_MAX, _lib.shape(1, h, n, d, m))
     qd, kd = to_bf16_dev(q), to_bf16_dev(k)  # held: ptr() of a temporary would let k reuse q's block
-    _lib.call("fga_cached_group_max", ptr(qd), ptr(kd), _lib.shape(1, h, n, d, m), 1, ptr(gmax), ptr(ws), stream())
+    _lib.call("fga_cached_group_max", ptr(qd), ptr(kd), _lib.shape(1, h, n, d, m), 1, ptr(gmax), ptr(ws), ws.numel(),
+              stream())
     torch.cuda.synchronize()
     got = gmax.cpu().numpy()
     mism = got != ref
