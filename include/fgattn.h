@@ -207,6 +207,20 @@ int fga_gather_rows(const void* matrix, int64_t rows, int64_t d, const int32_t* 
 int64_t fga_workspace_bytes(int op, fga_shape shape, int round_bf16);
 
 /*
+ * K2 of the attention kernel in isolation (test hook).  Runs the hot path's
+ * own gather producers (attn_ws.cu producer_half: 16-byte cp.async into the
+ * 128B-swizzled K/V ring slots) for one key list and copies every ring slot
+ * back out, un-swizzled, in chunk order: rows [0, c) of out_k / out_v equal
+ * gather_rows(k, idx[:c]) (sparse.py:95-108) bitwise, with c = min(*count,
+ * idx_stride); rows [c, 128*ceil(c/128)) are zero (the zero-filled tail of the
+ * last chunk).  Keys are clamped like the kernel's (min(unsigned key, n-1)).
+ *   k, v  : bf16 [n, d], d in {64, 128};  count : device int32[1];
+ *   out_k, out_v : bf16 [128*ceil(c/128), d].
+ */
+int fga_gather_ring_probe(const void* k, const void* v, int64_t n, int64_t d, const int32_t* idx, int64_t idx_stride,
+                          const int32_t* count, void* out_k, void* out_v, void* stream);
+
+/*
  * Average-query pooled scores (K1a, avg-query builder).  Replaces
  * masks.py:108-118 (pooled_query_scores):
  *   scores[b,h,g,j] = exp((k_j . mean_{i in g} q_i) * scale) / D   (fp32),

@@ -50,6 +50,7 @@ _SIGS = {
     "fga_tile_order": ([_P, FgaShape, _P, _P], _I),
     "fga_dense_attn_fwd": ([_P, _P, _P, _P, _I, _P, FgaShape, _P], _I),
     "fga_gather_rows": ([_P, _I64, _I64, _P, _I64, _P, _P], _I),
+    "fga_gather_ring_probe": ([_P, _P, _I64, _I64, _P, _I64, _P, _P, _P, _P], _I),
     "fga_workspace_bytes": ([_I, FgaShape, _I], _I64),
     "fga_pooled_scores": ([_P, _P, FgaShape, _I, _P, _P, _SZ, _P], _I),
     "fga_pooled_scores_bf16": ([_P, _P, FgaShape, _P, _P, _SZ, _P], _I),

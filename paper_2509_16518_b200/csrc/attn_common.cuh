@@ -145,6 +145,7 @@ __device__ __forceinline__ void store_row32(void* out, int64_t off, const uint32
 int launch_attn_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, int d, bool out_f32,
                    cudaStream_t stream);
 int launch_attn_dual(const CUtensorMap* maps, const AttnParams& p, int d, bool out_f32, cudaStream_t stream);
+int launch_ring_probe(const AttnParams& p, int d, void* out_k, void* out_v, cudaStream_t stream);
 
 // Producer-side memory safety.  The producers load their keys before waiting for a free ring
 // slot (the load latency hides behind the wait); clamp_key() then maps a listed key to

@@ -145,4 +145,24 @@ int launch_attn(const AttnLaunch& a, const fga_shape& s, cudaStream_t stream) {
   return dispatch(maps, a.q, a.k, a.v, p, static_cast<int>(D), f32, a.flags, stream);
 }
 
+int launch_gather_probe(const void* k, const void* v, int64_t n, int64_t d, const int32_t* idx, int64_t idx_stride,
+                        const int32_t* count, void* out_k, void* out_v, cudaStream_t stream) {
+  if (d != 64 && d != 128) return fail(FGA_EUNSUPPORTED, "gather probe: head_dim must be 64 or 128");
+  if (n < 1 || n >= (int64_t(1) << 31) || idx_stride < 1) return fail(FGA_EINVAL, "gather probe: bad n / stride");
+  AttnParams p{};
+  p.k = k;
+  p.v = v;
+  p.idx = idx;
+  p.idx_group_stride = idx_stride;
+  p.counts = count;
+  p.tile_begin = 0;
+  p.n_tiles = 1;
+  p.heads = 1;
+  p.seq_len = static_cast<int>(n);
+  p.group_size = static_cast<int>(n < BM ? n : BM);
+  p.groups = static_cast<int>((n + p.group_size - 1) / p.group_size);
+  p.tiles_per_group = 1;
+  return launch_ring_probe(p, static_cast<int>(d), out_k, out_v, stream);
+}
+
 }  // namespace fga

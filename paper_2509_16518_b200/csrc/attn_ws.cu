@@ -697,7 +697,65 @@ int launch_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, cudaS
   return check_launch("fga_attn_ws_kernel");
 }
 
+// ------------------------------------------------------------------ K2 in isolation
+// The hot path's own producer warps (producer_half, warps 10-13) filling the K and V rings for
+// one tile, with warp 0 standing in for the MMA issuers: it waits for each chunk's slots, copies
+// them out of the 128B swizzle into rows [128c, 128c + 128) of out_k / out_v and frees them.
+// Bitwise the packed tiles the tensor core reads (rows past the list end zero-filled), so the
+// gather is tested by itself (sparse.py:95-108), not only through the attention tolerance.
+template <int D>
+__global__ void __launch_bounds__(32 * NWARPS, 1)
+    fga_ring_probe_kernel(const AttnParams p, __nv_bfloat16* __restrict__ out_k, __nv_bfloat16* __restrict__ out_v) {
+  using L = WsSmem<D>;
+  extern __shared__ __align__(1024) uint8_t smem_ws[];
+  uint8_t* smem = smem_ws;
+  const Bars bar = carve_bars<D>(smem);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < NSK; ++i) { mbar_init(&bar.k_full[i], 64); mbar_init(&bar.k_empty[i], 1); }
+    for (int i = 0; i < NSV; ++i) { mbar_init(&bar.v_full[i], 64); mbar_init(&bar.v_empty[i], 1); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp >= WARP_PROD0 && warp < WARP_PROD0 + NPROD) {
+    producer_half<D>(p, nullptr, nullptr, smem, bar, (warp - WARP_PROD0) >> 1, (warp - WARP_PROD0) & 1, lane);
+  } else if (warp == 0) {
+    const Tile t = decode_tile(p, p.tile_begin);
+    for (int c = 0; c < t.nchunks; ++c) {
+      for (int kv = 0; kv < 2; ++kv) {
+        const int nslot = kv ? NSV : NSK;
+        const uint32_t slot = c % nslot, use = c / nslot;
+        mbar_wait(&(kv ? bar.v_full : bar.k_full)[slot], use & 1);
+        const uint8_t* ring = smem + (kv ? L::OFF_V : L::OFF_K) + slot * L::KV;
+        __nv_bfloat16* out = kv ? out_v : out_k;
+        for (int e = lane; e < BN * (D / 8); e += 32) {  // 16-byte pieces, row-major
+          const int r = e / (D / 8), pc = e % (D / 8), h = pc / 8, cc = pc % 8;
+          const uint4 x = *reinterpret_cast<const uint4*>(ring + h * HALF + r * 128 + ((cc ^ (r & 7)) << 4));
+          *reinterpret_cast<uint4*>(out + (static_cast<int64_t>(c) * BN + r) * D + pc * 8) = x;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&(kv ? bar.v_empty : bar.k_empty)[slot]);
+        __syncwarp();
+      }
+    }
+  }
+}
+
 }  // namespace
+
+int launch_ring_probe(const AttnParams& p, int d, void* out_k, void* out_v, cudaStream_t stream) {
+  const int smem = d == 64 ? WsSmem<64>::BYTES : WsSmem<128>::BYTES;
+  const void* fn = d == 64 ? reinterpret_cast<const void*>(fga_ring_probe_kernel<64>)
+                           : reinterpret_cast<const void*>(fga_ring_probe_kernel<128>);
+  if (const int rc = smem_opt_in(fn, smem, "ring_probe"); rc != FGA_OK) return rc;
+  auto* ok = static_cast<__nv_bfloat16*>(out_k);
+  auto* ov = static_cast<__nv_bfloat16*>(out_v);
+  if (d == 64)
+    fga_ring_probe_kernel<64><<<1, 32 * NWARPS, smem, stream>>>(p, ok, ov);
+  else
+    fga_ring_probe_kernel<128><<<1, 32 * NWARPS, smem, stream>>>(p, ok, ov);
+  return check_launch("fga_ring_probe_kernel");
+}
 
 int launch_attn_ws(const CUtensorMap* maps, const void* q, const AttnParams& p, int d, bool out_f32,
                    cudaStream_t stream) {

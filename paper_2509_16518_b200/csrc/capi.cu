@@ -279,6 +279,12 @@ int fga_pooled_scores(const void* q, const void* k, fga_shape shape, int round_b
   return launch_pooled_scores(q, k, shape, round_bf16, scores, nullptr, w, static_cast<cudaStream_t>(stream));
 }
 
+int fga_gather_ring_probe(const void* k, const void* v, int64_t n, int64_t d, const int32_t* idx, int64_t idx_stride,
+                          const int32_t* count, void* out_k, void* out_v, void* stream) {
+  if (!k || !v || !idx || !count || !out_k || !out_v) return fail(FGA_EINVAL, "null pointer");
+  return launch_gather_probe(k, v, n, d, idx, idx_stride, count, out_k, out_v, static_cast<cudaStream_t>(stream));
+}
+
 int fga_pooled_scores_bf16(const void* q, const void* k, fga_shape shape, uint16_t* scores, void* ws,
                            size_t ws_bytes, void* stream) {
   int rc = check_shape(shape);

@@ -1,10 +1,14 @@
-// K2 in isolation: the TMA tile::gather4 producer of the attention kernel,
-// writing the packed tile back to global memory so its bytes can be compared
-// bitwise with gather_rows (/root/reference/pkg/src/sliceattn/sparse.py:95-108).
+// gather_rows (/root/reference/pkg/src/sliceattn/sparse.py:95-108) on the TMA
+// tile::gather4 engine: the packed tile is written back to global memory so its
+// bytes can be compared bitwise with the reference.  This is the public gather
+// primitive, NOT the attention kernel's producer: the hot path gathers with
+// 16-byte cp.async from four producer warps (attn_ws.cu producer_half; tested by
+// itself through fga_gather_ring_probe), which measured faster than gather4 issued
+// from the producer warps (profiles/r02/gather4_vs_ldgsts.md).
 //
 // One CTA (one warp) per 128 indices.  Lane l gathers rows 4l..4l+3 of the
-// chunk with one gather4 per 64-column half into a 128B-swizzled stage --
-// exactly the smem image the MMA consumes -- then the warp un-swizzles it.
+// chunk with one gather4 per 64-column half into a 128B-swizzled stage (the
+// same SW128 image as the attention ring slots), then the warp un-swizzles it.
 #include "internal.h"
 #include "ptx.cuh"
 

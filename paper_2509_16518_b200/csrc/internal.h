@@ -69,6 +69,8 @@ size_t ws_cached_bytes(const fga_shape& s);
 
 // Launchers (attn_launch.cu / gather.cu / compact.cu / maskbuild.cu).
 int launch_attn(const AttnLaunch& a, const fga_shape& s, cudaStream_t stream);
+int launch_gather_probe(const void* k, const void* v, int64_t n, int64_t d, const int32_t* idx, int64_t idx_stride,
+                        const int32_t* count, void* out_k, void* out_v, cudaStream_t stream);
 int launch_gather(const void* matrix, int64_t rows, int64_t d, const int32_t* indices, int64_t n_idx, void* out,
                   cudaStream_t stream);
 int launch_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bits, cudaStream_t stream);
