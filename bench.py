@@ -760,6 +760,22 @@ def extras(args, torch, np, fga, cfg, q, k, v, keep, mask, out, kernel_ms, flush
             dense[name] = None
     best = min(x for x in dense.values() if x)
     dense["best_ms"] = best
+    # full mask (sparse.py:206-213): sparse_attention dispatches it to the contiguous-chunk kernel;
+    # the gather kernel on the same all-keys lists for comparison (FGA_DENSE_DISPATCH=0)
+    g_ = cfg.num_groups
+    fidx = torch.arange(n, dtype=torch.int32, device=q.device).expand(1, heads, g_, n).contiguous()
+    fmask = fga.DeviceIndexMask(1, heads, n, m, fidx, torch.full((1, heads, g_), n, dtype=torch.int32,
+                                                                 device=q.device), validated=True)
+    tf = timed_steps(torch, lambda: fga.sparse_attention(q, k, v, fmask, cfg), max(3, args.steps // 2), flush, stream)
+    os.environ["FGA_DENSE_DISPATCH"] = "0"
+    try:
+        tg = timed_steps(torch, lambda: fga.sparse_attention(q, k, v, fmask, cfg), max(3, args.steps // 2), flush,
+                         stream)
+    finally:
+        os.environ.pop("FGA_DENSE_DISPATCH", None)
+    dense["full_mask_dispatched_ms"] = sorted(tf)[len(tf) // 2]
+    dense["full_mask_gather_kernel_ms"] = sorted(tg)[len(tg) // 2]
+    del fidx, fmask
     dense["dense_flops"] = 4 * d * heads * n * n
     dense["shard"] = f"{heads} heads on this GPU" if world > 1 else "the whole layer"
     line["dense"] = dense

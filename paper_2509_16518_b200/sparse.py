@@ -156,6 +156,7 @@ class DeviceIndexMask:
     counts: object
     validated: bool = False
     _order: object = field(default=None, repr=False)
+    _full: object = field(default=None, repr=False)
 
     @property
     def num_groups(self) -> int:
@@ -401,7 +402,34 @@ def _check_precision(cfg: AttnConfig, *ts) -> None:
         "accumulation -- use AttnConfig(..., precision='bf16') or pass bf16 CUDA tensors")
 
 
-def _run_sparse(qd, kd, vd, dmask: DeviceIndexMask, cfg: AttnConfig, out_dtype, lse: bool):
+def _is_full(mask, dmask: DeviceIndexMask, cfg: AttnConfig) -> bool:
+    """Every group lists every key (full_mask, sparse.py:206-213): attention over the listed keys is
+    then dense attention, and the contiguous-chunk kernel (fga_dense_attn_fwd: TMA boxes, no index
+    reads, no gather) computes it with the same chunk order and arithmetic.  Host masks answer from
+    their counts; a device mask once per mask (one reduction + sync, cached)."""
+    if os.environ.get("FGA_DENSE_DISPATCH", "1") == "0":
+        return False
+    cells = cfg.batch * cfg.heads * cfg.num_groups * cfg.seq_len
+    if isinstance(mask, SparseIndexMask):
+        return mask.total_indices == cells
+    if dmask._full is None:
+        dmask._full = bool(dmask.validated and int(dmask.counts.sum(dtype=torch().int64).item()) == cells)
+    return dmask._full
+
+
+def _run_dense(qd, kd, vd, cfg: AttnConfig, out_dtype, lse: bool):
+    t = torch()
+    o = t.empty(cfg.dims, dtype=out_dtype, device=qd.device)
+    l = t.empty(cfg.dims[:3], dtype=t.float32, device=qd.device) if lse else None
+    _lib.call("fga_dense_attn_fwd", ptr(qd), ptr(kd), ptr(vd), ptr(o),
+              _lib.FGA_OUT_F32 if out_dtype == t.float32 else _lib.FGA_OUT_BF16, ptr(l),
+              _lib.shape(*cfg.dims, cfg.group_size, cfg.scale), stream_ptr())
+    return o, l
+
+
+def _run_sparse(qd, kd, vd, dmask: DeviceIndexMask, cfg: AttnConfig, out_dtype, lse: bool, full: bool = False):
+    if full:
+        return _run_dense(qd, kd, vd, cfg, out_dtype, lse)
     t = torch()
     o = t.empty(cfg.dims, dtype=out_dtype, device=qd.device)
     l = t.empty(cfg.dims[:3], dtype=t.float32, device=qd.device) if lse else None
@@ -439,7 +467,7 @@ def sparse_attention(q, k, v, mask, cfg: AttnConfig, trace: list | None = None, 
     qd, kd, vd = as_device_bf16(q), as_device_bf16(k), as_device_bf16(v)
     dmask = _as_device_mask(mask, cfg, qd.device.index)
     dt = t.float32 if host else (out_dtype or t.bfloat16)
-    o, l = _run_sparse(qd, kd, vd, dmask, cfg, dt, return_lse)
+    o, l = _run_sparse(qd, kd, vd, dmask, cfg, dt, return_lse, full=_is_full(mask, dmask, cfg))
     if trace is not None:
         counts = mask.counts() if isinstance(mask, SparseIndexMask) else dmask.counts.cpu().numpy()
         trace.extend(chunk_trace(counts, cfg, chunk, GATHER))

@@ -272,3 +272,36 @@ def test_online_softmax_primitives_match_one_shot_softmax():
         fga.finalize(fga.init_state(2, 4))
     with pytest.raises(fga.ShapeError):
         fga.online_softmax_update(fga.init_state(2, 4), np.zeros((2, 3), np.float32), np.zeros((2, 4), np.float32))
+
+
+@pytest.mark.parametrize("n,m", [(1000, 128), (640, 256)])
+def test_full_mask_dispatches_to_the_dense_kernel(n, m, monkeypatch):
+    # full_mask == dense (sparse.py:206-213): sparse_attention routes a full mask to the
+    # contiguous-chunk kernel -- bitwise the same as flash_attention -- and the gather kernel on the
+    # same all-keys lists agrees (same chunk order)
+    cfg = fga.AttnConfig(1, 2, n, 128, group_size=m, precision="bf16")
+    g = torch.Generator(device="cuda").manual_seed(n)
+    q, k, v = (torch.randn(cfg.dims, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    gc = cfg.num_groups
+    fidx = torch.arange(n, dtype=torch.int32, device="cuda").expand(1, 2, gc, n).contiguous()
+    cnt = torch.full((1, 2, gc), n, dtype=torch.int32, device="cuda")
+    dm = fga.DeviceIndexMask(1, 2, n, m, fidx, cnt, validated=True)
+    o_disp = fga.sparse_attention(q, k, v, dm, cfg, out_dtype=torch.float32)
+    o_dense = fga.flash_attention(q, k, v, cfg, out_dtype=torch.float32)
+    assert torch.equal(o_disp, o_dense)
+    host = fga.sparse_attention(*(fga.new_tensor(cfg, "from_data", data=x.float().cpu().numpy()) for x in (q, k, v)),
+                                fga.full_mask(cfg), cfg)
+    assert np.array_equal(host.data, o_dense.cpu().numpy())
+    monkeypatch.setenv("FGA_DENSE_DISPATCH", "0")
+    o_gather = fga.sparse_attention(q, k, v, fga.DeviceIndexMask(1, 2, n, m, fidx, cnt, validated=True), cfg,
+                                    out_dtype=torch.float32)
+    # M <= 128: the same per-tile kernel with gathered chunks; M = 256: the dual-tile kernel (64-key
+    # halves), equal within the bf16 tolerance
+    assert (o_gather - o_dense).abs().max().item() <= (1e-5 if m <= 128 else ATOL)
+    # a mask one key short of full is not dense
+    cnt2 = cnt.clone()
+    cnt2[0, 1, 0] = n - 1
+    monkeypatch.delenv("FGA_DENSE_DISPATCH")
+    o_part = fga.sparse_attention(q, k, v, fga.DeviceIndexMask(1, 2, n, m, fidx, cnt2, validated=True), cfg,
+                                  out_dtype=torch.float32)
+    assert not torch.equal(o_part[0, 1, :m], o_dense[0, 1, :m]) and torch.equal(o_part[0, 0], o_dense[0, 0])
