@@ -881,6 +881,29 @@ def variable_mask_leg(torch, fga, cfg, q, k, v, flush, stream):
     # ideal: the pairs spread evenly over the SMs at the dynamic run's pair rate -> the tail is
     # the time the last CTAs run alone; static / dynamic shows what the scheduler recovers
     res["static_over_dynamic"] = res["static_ms"] / res["dynamic_ms"]
+    # per-CTA timeline of one launch each (fga_sparse_attn_fwd_timed, %globaltimer at CTA start / end):
+    # tail fraction = longest CTA / mean CTA (1.0 = perfectly balanced)
+    from paper_2509_16518_b200 import _lib
+
+    sms = torch.cuda.get_device_properties(q.device).multi_processor_count
+    buf = torch.zeros(2 * sms, dtype=torch.int64, device=q.device)
+    o = torch.empty_like(q)
+    shp = _lib.shape(*cfg.dims, cfg.group_size, cfg.scale)
+    for name, flags, order in (("dynamic", 0, mask.tile_order(cfg)), ("static", _lib.FGA_ATTN_STATIC, None)):
+        for _ in range(2):  # the second launch is the one kept (warm)
+            flush.zero_()
+            buf.zero_()
+            _lib.call("fga_sparse_attn_fwd_timed", q.data_ptr(), k.data_ptr(), v.data_ptr(), mask.idx.data_ptr(),
+                      mask.stride, mask.counts.data_ptr(), o.data_ptr(), _lib.FGA_OUT_BF16, None, shp, 0, -1,
+                      None if order is None else order.data_ptr(), None, flags, buf.data_ptr(), buf.numel(),
+                      stream.cuda_stream)
+        torch.cuda.synchronize()
+        t = buf.view(-1, 2).double()
+        t = t[t[:, 1] > 0]
+        busy = (t[:, 1] - t[:, 0]) / 1e6
+        res[f"{name}_cta_tail_fraction"] = float(busy.max() / busy.mean())
+        res[f"{name}_cta_ms"] = {"mean": float(busy.mean()), "max": float(busy.max()), "min": float(busy.min()),
+                                 "makespan": float((t[:, 1].max() - t[:, 0].min()) / 1e6), "ctas": int(t.shape[0])}
     return res
 
 

@@ -158,6 +158,17 @@ int fga_sparse_attn_fwd_ex(const void* q, const void* k, const void* v, const in
                            int32_t* status, int flags, void* stream);
 
 /*
+ * fga_sparse_attn_fwd_ex plus a per-CTA timeline of the persistent kernel
+ * (load-balance measurement): cta_ns[2b] / cta_ns[2b + 1] = %globaltimer (ns)
+ * when CTA b starts / finishes its tiles, for b < cta_ns_len / 2 (device
+ * int64 buffer; the grid is at most one CTA per SM).
+ */
+int fga_sparse_attn_fwd_timed(const void* q, const void* k, const void* v, const int32_t* idx,
+                              int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
+                              fga_shape shape, int64_t tile_begin, int64_t tile_end, const int32_t* order,
+                              int32_t* status, int flags, long long* cta_ns, int64_t cta_ns_len, void* stream);
+
+/*
  * Checks an index mask against the SparseIndexMask invariants
  * (sparse.py:36-52): 1 <= counts[r] <= idx_group_stride, keys in [0, n),
  * strictly ascending.  Synchronises `stream`; returns FGA_OK, FGA_EINVAL

@@ -46,6 +46,8 @@ _SIGS = {
     "fga_sparse_attn_fwd": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _P], _I),
     "fga_sparse_attn_fwd_tiles": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _I64, _I64, _P], _I),
     "fga_sparse_attn_fwd_ex": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _I64, _I64, _P, _P, _I, _P], _I),
+    "fga_sparse_attn_fwd_timed": ([_P, _P, _P, _P, _I64, _P, _P, _I, _P, FgaShape, _I64, _I64, _P, _P, _I, _P, _I64,
+                                   _P], _I),
     "fga_validate_mask": ([_P, _I64, _P, _I64, _I64, _P, _P], _I),
     "fga_tile_order": ([_P, FgaShape, _P, _P], _I),
     "fga_dense_attn_fwd": ([_P, _P, _P, _P, _I, _P, FgaShape, _P], _I),

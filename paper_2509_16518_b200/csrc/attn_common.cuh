@@ -15,6 +15,12 @@ constexpr int BM = 128;         // query rows per tile (UMMA M)
 constexpr int BN = 128;         // keys per chunk
 constexpr int HALF = BM * 128;  // one SW128 block: 128 rows x 64 bf16 = 16 KB
 
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct AttnParams {
   const void* k;  // raw bf16 [B*H*N, D] (cp.async gather source)
   const void* v;
@@ -33,7 +39,13 @@ struct AttnParams {
   int32_t* status;       // nullable device word: FGA_STATUS_* bits of mask violations seen (atomicOr)
   unsigned int* sched;   // dynamic tile counter (self-resetting, attn_ws.cu); null = static stride
   const int32_t* order;  // nullable: work index -> tile offset from tile_begin (LPT order)
+  long long* cta_ns;     // nullable: %globaltimer at start / end of CTA b in [2b], [2b + 1] (b < cta_ns_len / 2)
+  int64_t cta_ns_len;
 };
+__device__ __forceinline__ void record_cta_ns(const AttnParams& p, int end) {
+  if (p.cta_ns != nullptr && threadIdx.x == 0 && 2 * static_cast<int64_t>(blockIdx.x) + 1 < p.cta_ns_len)
+    p.cta_ns[2 * blockIdx.x + end] = global_ns();
+}
 
 // Mask violations the kernels detect while running are ORed into p.status as the FGA_STATUS_*
 // bits of fgattn.h (sparse.py:47-52 raises for these).  The kernels stay memory-safe: counts are
@@ -77,11 +89,6 @@ struct AttnParams {
   do {                      \
   } while (0)
 #endif
-__device__ __forceinline__ long long global_ns() {
-  long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 // One work tile: <=128 query rows of group (b,h,g) and that group's key list.
 struct Tile {

@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  record_cta_ns(p, 0);
   tc_fence_after();
   const uint32_t tmem = *bar.tmem_slot;
   constexpr int kThreads = 32 * NWARPS;
@@ -494,6 +495,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  record_cta_ns(p, 1);
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);

@@ -123,6 +123,8 @@ int launch_attn(const AttnLaunch& a, const fga_shape& s, cudaStream_t stream) {
   p.dense = dense ? 1 : 0;
   p.status = a.status;
   p.order = a.order;
+  p.cta_ns = a.cta_ns;
+  p.cta_ns_len = a.cta_ns != nullptr ? a.cta_ns_len : 0;
   if (!(a.flags & FGA_ATTN_STATIC) && !dual) {
     p.sched = sched_slot();
     if (p.sched == nullptr) return fail(FGA_ECUDA, "scheduler counters unavailable");

@@ -655,6 +655,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
   tc_fence_after();
   const uint32_t tmem = *bar.tmem_slot;
   if (p.trace != nullptr && tid == 0 && blockIdx.x < 1024) p.trace[FGA_TRACE_CTA_OFF + 2 * blockIdx.x] = global_ns();
+  record_cta_ns(p, 0);
 
   static_assert(NWARPS % 4 == 0, "whole warpgroups are needed for setmaxnreg");
   // setmaxnreg.inc can only take registers this CTA released with .dec (its pool is threads x launch regs)
@@ -678,6 +679,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
   tc_fence_before();
   __syncthreads();
   if (p.trace != nullptr && tid == 0 && blockIdx.x < 1024) p.trace[FGA_TRACE_CTA_OFF + 2 * blockIdx.x + 1] = global_ns();
+  record_cta_ns(p, 1);
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);

@@ -150,6 +150,14 @@ int fga_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, i
 int fga_sparse_attn_fwd_ex(const void* q, const void* k, const void* v, const int32_t* idx, int64_t idx_group_stride,
                            const int32_t* counts, void* o, int o_dtype, float* lse, fga_shape shape, int64_t tile_begin,
                            int64_t tile_end, const int32_t* order, int32_t* status, int flags, void* stream) {
+  return fga_sparse_attn_fwd_timed(q, k, v, idx, idx_group_stride, counts, o, o_dtype, lse, shape, tile_begin, tile_end,
+                                   order, status, flags, nullptr, 0, stream);
+}
+
+int fga_sparse_attn_fwd_timed(const void* q, const void* k, const void* v, const int32_t* idx,
+                              int64_t idx_group_stride, const int32_t* counts, void* o, int o_dtype, float* lse,
+                              fga_shape shape, int64_t tile_begin, int64_t tile_end, const int32_t* order,
+                              int32_t* status, int flags, long long* cta_ns, int64_t cta_ns_len, void* stream) {
   int rc = check_shape(shape);
   if (rc != FGA_OK) return rc;
   if (!q || !k || !v || !idx || !counts || !o) return fail(FGA_EINVAL, "null pointer");
@@ -185,6 +193,8 @@ int fga_sparse_attn_fwd_ex(const void* q, const void* k, const void* v, const in
   a.order = order;
   a.status = status;
   a.flags = flags;
+  a.cta_ns = cta_ns;
+  a.cta_ns_len = cta_ns_len;
   rc = launch_attn(a, shape, st);
   if (rc != FGA_OK || !(flags & FGA_ATTN_CHECK)) return rc;
   return status_to_code(status, st, "fga_sparse_attn_fwd_ex");

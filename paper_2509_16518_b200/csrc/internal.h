@@ -43,6 +43,8 @@ struct AttnLaunch {
   const int32_t* order = nullptr;
   int32_t* status = nullptr;
   int flags = 0;
+  long long* cta_ns = nullptr;
+  int64_t cta_ns_len = 0;
 };
 
 // Caller-provided device workspace (the C ABI never allocates): take() carves 256-byte aligned
