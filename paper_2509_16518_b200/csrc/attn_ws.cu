@@ -80,6 +80,12 @@ constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
 #ifndef FGA_NOEXP
 #define FGA_NOEXP 0  // P = S bits, no exp
 #endif
+#ifndef FGA_POLY
+#define FGA_POLY 0  // A/B knob: every FGA_POLY-th exp pair on the FMA pipe (0: all on MUFU)
+#endif
+#ifndef FGA_POLY_DEG
+#define FGA_POLY_DEG 3
+#endif
 
 template <int D>
 struct WsSmem {
@@ -410,7 +416,11 @@ __device__ __forceinline__ void exp_chunk(const uint32_t (&sv)[2][32], float sl2
       for (int r = 0; r < 2; ++r) {
         const float2 sx = make_float2(__uint_as_float(sv[hh][4 * k + 2 * r]), __uint_as_float(sv[hh][4 * k + 2 * r + 1]));
         const float2 x = __ffma2_rn(sx, sc2, nm[r]);
-        const float2 pr = make_float2(ex2(x.x), ex2(x.y));
+        // A/B knob FGA_POLY = p > 0: every p-th pair on the FMA pipe (ex2_poly2), the rest on MUFU
+        constexpr int PP = FGA_POLY > 0 ? FGA_POLY : 1;
+        const float2 pr = (FGA_POLY > 0 && (16 * hh + 2 * k + r) % PP == PP - 1)
+                              ? ex2_poly2<FGA_POLY_DEG>(x)
+                              : make_float2(ex2(x.x), ex2(x.y));
         sum2[r][k & 1] = __fadd2_rn(sum2[r][k & 1], pr);
         pk[2 * (8 * hh + k) + r] = pack_bf16(pr.x, pr.y);
       }
