@@ -286,7 +286,9 @@ int fga_pooled_scores(const void* q, const void* k, fga_shape shape, int round_b
   if (!q || !k || !scores) return fail(FGA_EINVAL, "null pointer");
   if ((rc = check_ws(ws)) != FGA_OK) return rc;
   Workspace w(ws, ws_bytes);
-  return launch_pooled_scores(q, k, shape, round_bf16, scores, nullptr, w, static_cast<cudaStream_t>(stream));
+  PooledOut out;
+  out.scores = scores;
+  return launch_pooled_scores(q, k, shape, round_bf16, out, w, static_cast<cudaStream_t>(stream));
 }
 
 int fga_gather_ring_probe(const void* k, const void* v, int64_t n, int64_t d, const int32_t* idx, int64_t idx_stride,
@@ -302,7 +304,9 @@ int fga_pooled_scores_bf16(const void* q, const void* k, fga_shape shape, uint16
   if (!q || !k || !scores) return fail(FGA_EINVAL, "null pointer");
   if ((rc = check_ws(ws)) != FGA_OK) return rc;
   Workspace w(ws, ws_bytes);
-  return launch_pooled_scores(q, k, shape, 1, nullptr, scores, w, static_cast<cudaStream_t>(stream));
+  PooledOut out;
+  out.scores16 = scores;
+  return launch_pooled_scores(q, k, shape, 1, out, w, static_cast<cudaStream_t>(stream));
 }
 
 int fga_select_compact(const uint16_t* scores, int64_t rows, int64_t n, int mode, float tau, int64_t top_k,
@@ -328,12 +332,29 @@ int fga_build_mask_avgq(const void* q, const void* k, fga_shape shape, int strat
   const int64_t G = (shape.seq_len + shape.group_size - 1) / shape.group_size;
   const int64_t rows = shape.batch * shape.heads * G, n = shape.seq_len;
   Workspace w(ws, ws_bytes);
+  if (round_bf16 && strategy == FGA_SELECT_THRESHOLD && (shape.head_dim == 64 || shape.head_dim == 128)) {
+    // threshold decided in the tensor-core score epilogue: keep bits + argmax, no score tensor
+    Workspace pw = w;
+    pw.take<char>(static_cast<int64_t>(ws_pooled_bytes(shape)));
+    const int64_t words = (n + 31) / 32;
+    PooledOut out;
+    out.keep_bits = pw.take<uint32_t>(rows * words);
+    out.amax = pw.take<unsigned long long>(rows);
+    out.tau = tau;
+    if (out.keep_bits == nullptr || out.amax == nullptr)
+      return fail(FGA_EINVAL, "build_mask_avgq: workspace too small (fga_workspace_bytes)");
+    if (cudaMemsetAsync(out.amax, 0, sizeof(unsigned long long) * rows, st) != cudaSuccess) return check_launch("memset");
+    if ((rc = launch_pooled_scores(q, k, shape, 1, out, w, st)) != FGA_OK) return rc;
+    return launch_compact_bits(out.keep_bits, rows, n, idx, idx_stride, counts, fill_sentinel, st, out.amax);
+  }
   if (round_bf16 && n <= FGA_SELECT_MAX_N) {  // bf16 scores -> fused selection + compaction
     Workspace pw = w;
     pw.take<char>(static_cast<int64_t>(ws_pooled_bytes(shape)));
     uint16_t* s16 = pw.take<uint16_t>(rows * n);
     if (s16 == nullptr) return fail(FGA_EINVAL, "build_mask_avgq: workspace too small (fga_workspace_bytes)");
-    if ((rc = launch_pooled_scores(q, k, shape, 1, nullptr, s16, w, st)) != FGA_OK) return rc;
+    PooledOut out;
+    out.scores16 = s16;
+    if ((rc = launch_pooled_scores(q, k, shape, 1, out, w, st)) != FGA_OK) return rc;
     return launch_select_compact(s16, rows, n, strategy, tau, top_k, idx, idx_stride, counts, fill_sentinel, st);
   }
   Workspace pw = w;
@@ -341,7 +362,9 @@ int fga_build_mask_avgq(const void* q, const void* k, fga_shape shape, int strat
   float* sc = pw.take<float>(rows * n);
   uint8_t* keep = pw.take<uint8_t>(rows * n);
   if (sc == nullptr || keep == nullptr) return fail(FGA_EINVAL, "build_mask_avgq: workspace too small (fga_workspace_bytes)");
-  if ((rc = launch_pooled_scores(q, k, shape, round_bf16, sc, nullptr, w, st)) != FGA_OK) return rc;
+  PooledOut out;
+  out.scores = sc;
+  if ((rc = launch_pooled_scores(q, k, shape, round_bf16, out, w, st)) != FGA_OK) return rc;
   if (strategy == FGA_SELECT_THRESHOLD) {
     if ((rc = launch_threshold(sc, rows * n, tau, keep, st)) != FGA_OK) return rc;
     return launch_compact(keep, sc, rows, n, idx, idx_stride, counts, fill_sentinel, st);

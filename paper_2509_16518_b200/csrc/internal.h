@@ -77,15 +77,26 @@ int launch_gather(const void* matrix, int64_t rows, int64_t d, const int32_t* in
                   cudaStream_t stream);
 int launch_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bits, cudaStream_t stream);
 int launch_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx, int64_t idx_stride,
-                        int32_t* counts, int fill, cudaStream_t stream);
+                        int32_t* counts, int fill, cudaStream_t stream, const unsigned long long* amax = nullptr);
 int launch_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, int64_t n, int32_t* idx,
                        int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream);
 int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s, int round, float* gmax,
                                float* row_max, float* row_rinv, cudaStream_t st);
+// Outputs of the avg-query pooled-score pass (exactly one of scores / scores16 / keep_bits):
+// fp32 scores, bf16 scores, or the threshold decision fused into the epilogue -- keep bits
+// (bit b of word w of row r = key 32w + b) plus amax[r] = max over the row of
+// (order-preserving bf16 key << 32 | ~key index), the argmax fallback (callers zero amax first).
+struct PooledOut {
+  float* scores = nullptr;
+  uint16_t* scores16 = nullptr;
+  uint32_t* keep_bits = nullptr;
+  unsigned long long* amax = nullptr;
+  float tau = 0.f;
+};
 int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, const void* k, const fga_shape& s, int round,
-                            float* scores, uint16_t* scores16, cudaStream_t st);
-int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, float* scores,
-                         uint16_t* scores16, Workspace& ws, cudaStream_t st);
+                            const PooledOut& out, cudaStream_t st);
+int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, const PooledOut& out,
+                         Workspace& ws, cudaStream_t st);
 int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, Workspace& ws,
                             cudaStream_t st);
 int launch_threshold(const float* s, int64_t n, float tau, uint8_t* keep, cudaStream_t st);

@@ -520,8 +520,8 @@ size_t ws_cached_bytes(const fga_shape& s) {
   return Workspace::align(sizeof(float) * rows) + Workspace::align(sizeof(double) * rows);
 }
 
-int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, float* scores,
-                         uint16_t* scores16, Workspace& ws, cudaStream_t st) {
+int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, const PooledOut& out,
+                         Workspace& ws, cudaStream_t st) {
   const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
   const int64_t G = (N + M - 1) / M;
   if (D % DK != 0) return fail(FGA_EUNSUPPORTED, "pooled_scores: head_dim must be a multiple of 32");
@@ -543,14 +543,14 @@ int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int r
         static_cast<int>(G));
   }
   const char* cc = std::getenv("FGA_POOLED_CC");  // 1: the CUDA-core tile kernel below
-  if (cc == nullptr || cc[0] != '1') {
-    const int rc = launch_pooled_scores_tc(qbar, parts, k, s, round, scores, scores16, st);
-    if (rc != FGA_EUNSUPPORTED) return rc;
+  if (out.keep_bits != nullptr || cc == nullptr || cc[0] != '1') {
+    const int rc = launch_pooled_scores_tc(qbar, parts, k, s, round, out, st);
+    if (rc != FGA_EUNSUPPORTED || out.keep_bits != nullptr) return rc;  // fused bits: tensor-core pass only
   }
   const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
   dim3 grid(static_cast<unsigned>((N + PT - 1) / PT), static_cast<unsigned>((G + PT - 1) / PT),
             static_cast<unsigned>(B * H));
-  pooled_scores128_kernel<<<grid, 256, 0, st>>>(qbar, static_cast<const __nv_bfloat16*>(k), scores, scores16,
+  pooled_scores128_kernel<<<grid, 256, 0, st>>>(qbar, static_cast<const __nv_bfloat16*>(k), out.scores, out.scores16,
                                                 static_cast<int>(N), static_cast<int>(D), static_cast<int>(G), scale,
                                                 round);
   return check_launch("pooled_scores128_kernel");

@@ -93,7 +93,11 @@ struct CbParams {
   int groups;   // pass 2: G
   int64_t part_rows;  // pass 2: rows of one q̄ part (B*H*G)
   float* scores;      // pass 2: [B*H*G*N] fp32, or
-  uint16_t* scores16; // pass 2: [B*H*G*N] bf16 bits (the builders' input; p.round must be 1)
+  uint16_t* scores16; // pass 2: [B*H*G*N] bf16 bits (the builders' input; p.round must be 1), or
+  uint32_t* keep_bits;            // pass 2: [B*H*G, words] threshold decisions (bf16 score >= tau)
+  unsigned long long* amax;       // pass 2 with keep_bits: [B*H*G] argmax key per row (atomicMax)
+  float tau;
+  int words;                      // ceil(N / 32)
   int kslabs;         // pass 2: key ranges per (b*h, group tile)
   float scale;
   int round;
@@ -225,6 +229,14 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
     const int row = q * 32 + lane;  // TMEM lane: query row (pass 0) or key row (pass 1)
     const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16) + w * 32;
     const float4* tab = reinterpret_cast<const float4*>(smem + L::OFF_TAB);
+    const float scale = p.scale;  // parameters hoisted into registers for the per-score loops
+    const int rnd = p.round;
+    const int n_keys = p.n;
+    uint16_t* const s16 = p.scores16;
+    float* const s32 = p.scores;
+    uint32_t* const bits_out = p.keep_bits;
+    const uint32_t tau_b16 = __bfloat16_as_ushort(__float2bfloat16_ru(p.tau));  // p.tau > 0
+    (void)rnd; (void)s16; (void)s32; (void)bits_out; (void)tau_b16;
     uint32_t sc = 0;
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
       int64_t bh;
@@ -267,23 +279,59 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
           // s = exp(k_j . q̄_g * scale) / D, bf16-rounded
           const int j = c * BN + row;
           constexpr float inv_d = 1.0f / D;  // D is a power of two: x / D == x * (1/D) exactly
-          if (j < p.n) {
-            const int64_t off = (bh * p.groups + t * BM + w * 32) * static_cast<int64_t>(p.n) + j;
+          if (bits_out != nullptr || j < n_keys) {
+            if (j >= n_keys) {  // keys past N: never kept, never the argmax
+#pragma unroll
+              for (int k = 0; k < 32; ++k) v[k] = __float_as_uint(-INFINITY);
+            }
+            const int64_t off = (bh * p.groups + t * BM + w * 32) * static_cast<int64_t>(n_keys) + j;
             const int kmax = min(32, p.groups - (t * BM + w * 32));
-            if (p.scores16 != nullptr) {
+            // s = fl(fl(expf(fl(acc * scale))) / D); one pointer step of n per group column, no
+            // per-element predicate for a full 32-group slice
+            if (bits_out != nullptr) {
+              // threshold fused into the epilogue (masks.py:131-132): per group column one ballot of
+              // this warp's 32 consecutive keys -> keep word; the bf16 score's order-preserving key
+              // and the key index reduced for the argmax fallback (masks.py:86-87)
+              const int g0 = t * BM + w * 32;
+              uint32_t myword = 0, mybest = 0;
 #pragma unroll
-              for (int k = 0; k < 32; ++k)
-                if (k < kmax)
-                  p.scores16[off + static_cast<int64_t>(k) * p.n] = __bfloat16_as_ushort(
-                      __float2bfloat16_rn(__fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), p.scale)), inv_d)));
-            } else {
-              float* dst = p.scores + off;
-#pragma unroll
+              // scores are exp(.)/D >= 0 (or NaN), so their bf16 bits order like their values and
+              // s >= tau <=> bits >= bits(tau rounded up to bf16)
               for (int k = 0; k < 32; ++k) {
+                const uint32_t b16 = __bfloat16_as_ushort(
+                    __float2bfloat16_rn(__fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), scale)), inv_d)));
+                const uint32_t word = __ballot_sync(0xffffffffu, b16 >= tau_b16 && b16 <= 0x7F80u);
+                const uint32_t best = __reduce_max_sync(0xffffffffu, (b16 << 16) | (31u - lane));
+                if (lane == k) { myword = word; mybest = best; }
+              }
+              const int g = g0 + lane;
+              if (g < p.groups && c * BN + q * 32 < n_keys) {  // a word past N belongs to no row
+                const int64_t row_g = bh * p.groups + g;
+                bits_out[row_g * p.words + (c * BN + q * 32) / 32] = myword;
+                const uint32_t jb = static_cast<uint32_t>(c * BN + q * 32) + (31u - (mybest & 31u));
+                atomicMax(p.amax + row_g, (static_cast<unsigned long long>((mybest >> 16) | 0x8000u) << 32) |
+                                              (0xFFFFFFFFu - jb));
+              }
+            } else if (s16 != nullptr) {
+              uint16_t* dst = s16 + off;
+              if (kmax == 32) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k, dst += n_keys)
+                  *dst = __bfloat16_as_ushort(__float2bfloat16_rn(__fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), scale)), inv_d)));
+              } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k, dst += n_keys)
+                  if (k < kmax)
+                    *dst = __bfloat16_as_ushort(__float2bfloat16_rn(__fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), scale)), inv_d)));
+              }
+            } else {
+              float* dst = s32 + off;
+#pragma unroll
+              for (int k = 0; k < 32; ++k, dst += n_keys) {
                 if (k < kmax) {
-                  float sc = __fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), p.scale)), inv_d);
-                  if (p.round) sc = __bfloat162float(__float2bfloat16_rn(sc));
-                  dst[static_cast<int64_t>(k) * p.n] = sc;
+                  float sc = __fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), scale)), inv_d);
+                  if (rnd) sc = __bfloat162float(__float2bfloat16_rn(sc));
+                  *dst = sc;
                 }
               }
             }
@@ -476,7 +524,7 @@ __global__ void split3_kernel(const float* __restrict__ x, __nv_bfloat16* __rest
 // Avg-query scores s[b,h,g,j] = exp(k_j . q̄_g * scale) / D on the tensor cores (pass 2);
 // FGA_EUNSUPPORTED unless D is 64 or 128.  qbar: fp32 [B*H*G, D] (pooled_mean_kernel).
 int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, const void* k, const fga_shape& s, int round,
-                            float* scores, uint16_t* scores16, cudaStream_t st) {
+                            const PooledOut& out, cudaStream_t st) {
   const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
   if (D != 64 && D != 128) return FGA_EUNSUPPORTED;
   const int64_t G = (N + M - 1) / M;
@@ -496,8 +544,12 @@ int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, const void*
     p.nch = static_cast<int>((N + BN - 1) / BN);
     p.groups = static_cast<int>(G);
     p.part_rows = qrows;
-    p.scores = scores;
-    p.scores16 = scores16;
+    p.scores = out.scores;
+    p.scores16 = out.scores16;
+    p.keep_bits = out.keep_bits;
+    p.amax = out.amax;
+    p.tau = out.tau;
+    p.words = static_cast<int>((N + 31) / 32);
     // enough (b*h, group tile, key range) units for every SM, each at least 8 key chunks
     p.kslabs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(p.nch / 8, (4 * 148 + p.bh * p.tiles - 1) / (p.bh * p.tiles))));
     p.scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));

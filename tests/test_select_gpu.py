@@ -170,3 +170,25 @@ def test_build_mask_cached_single_call_equals_composition():
     rows = gmax.reshape(counts.size, -1)
     for r in range(counts.size):
         assert np.array_equal(idx[r, :counts[r]], _ref_threshold(rows[r], np.float32(tau))), r
+
+
+@pytest.mark.parametrize("n,d", [(1000, 128), (200, 64), (4100, 128)])
+def test_fused_threshold_builder_bits_and_fallback(n, d):
+    # threshold decided in the pooled-score epilogue (keep bits + argmax, fga_build_mask_avgq):
+    # bit-exact with the reference selection on the same (bf16) scores, ragged N, 30% of the groups
+    # empty -> argmax fallback (masks.py:86-87)
+    cfg = fga.AttnConfig(1, 3, n, d, precision="bf16")
+    g = torch.Generator(device="cuda").manual_seed(n + d)
+    q, k = (torch.randn(cfg.dims, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2))
+    scores = fga.pooled_query_scores(q, k, cfg).cpu().numpy()
+    rows = scores.reshape(-1, n)
+    tau = float(np.quantile(rows.max(-1), 0.3)) * 1.0001
+    m = fga.build_mask_avg_query(q, k, cfg, fga.MaskBuilderConfig("avg_query_threshold", tau=tau), device_result=True)
+    counts = m.counts.cpu().numpy().reshape(-1)
+    idx = m.idx.cpu().numpy().reshape(counts.size, -1)
+    fallbacks = 0
+    for r in range(counts.size):
+        ref = _ref_threshold(rows[r], np.float32(tau))
+        fallbacks += int((rows[r] >= np.float32(tau)).sum() == 0)
+        assert np.array_equal(idx[r, :counts[r]], ref), r
+    assert fallbacks > 0
