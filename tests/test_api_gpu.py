@@ -87,7 +87,7 @@ def test_avg_query_builders_match_reference(golden):
     cfg = cfg_of(g)
     q, k, _ = tensors(g, cfg)
     scores = fga.pooled_query_scores(q, k, cfg)
-    assert (scores != g["scores"]).mean() < 1e-3
+    assert (scores != g["scores"]).sum() <= max(2, 1e-4 * scores.size)
     thr = fga.build_mask_avg_query(q, k, cfg, fga.MaskBuilderConfig("avg_query_threshold", tau=float(g["tau"])))
     ref = g.lists()
     diff = [r for r in range(len(ref)) if not np.array_equal(thr._lists[r], ref[r])]

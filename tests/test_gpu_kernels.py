@@ -342,7 +342,8 @@ def test_pooled_scores_and_threshold_keep(golden):
     got = s.cpu().numpy()
     # scores are bf16-rounded fp32 dot products: equal except at rare rounding boundaries
     mism = got != ref
-    assert mism.mean() < 1e-3
+    print(f"pooled scores (golden): {mism.mean():.2e} of the bf16 values differ")
+    assert mism.sum() <= max(2, 1e-4 * mism.size)  # measured 0 here, 1.2e-5 at N = 32760
     assert np.abs(got - ref)[mism].max(initial=0) <= np.abs(ref).max() * 2 ** -7
     flips = (keep.cpu().numpy() != (ref >= tau))
     assert (flips <= mism).all()   # a keep bit can only flip where the score itself differs
@@ -367,7 +368,8 @@ def test_pooled_scores_tensor_cores_vs_oracle(n, d, h, m, monkeypatch):
         torch.cuda.synchronize()
         got = s.cpu().numpy()
         mism = got != ref
-        assert mism.mean() < 1e-3, (cc, mism.mean())
+        print(f"pooled scores n={n} d={d} cc={cc}: {mism.mean():.2e} of the bf16 values differ")
+        assert mism.sum() <= max(2, 1e-4 * mism.size), (cc, mism.mean())
         assert np.abs(got - ref)[mism].max(initial=0) <= np.abs(ref).max() * 2 ** -7, cc
 
 
@@ -400,7 +402,8 @@ def test_cached_group_max(golden):
     got = gmax.cpu().numpy()
     ref = g["gmax"]
     mism = got != ref
-    assert mism.mean() < 1e-3
+    print(f"cached group max (golden): {mism.mean():.2e} of the bf16 values differ")
+    assert mism.sum() <= max(2, 1e-4 * mism.size)  # measured 1 value of 4096
     tau = float(g["tau"])
     flips = (got >= tau) != (ref >= tau)
     assert (flips <= mism).all()
@@ -427,7 +430,8 @@ def test_cached_group_max_tensor_cores_vs_oracle(n, d, h, monkeypatch):
         torch.cuda.synchronize()
         got = gmax.cpu().numpy()
         mism = got != ref
-        assert mism.mean() < 1e-3, (cc, mism.mean())
+        print(f"cached group max n={n} d={d} cc={cc}: {mism.mean():.2e} of the bf16 values differ")
+        assert mism.sum() <= max(2, 1e-4 * mism.size), (cc, mism.mean())
         # where they differ, by one bf16 step at most
         if mism.any():
             rel = np.abs(got[mism] - ref[mism]) / np.maximum(np.abs(ref[mism]), 1e-30)
@@ -451,7 +455,7 @@ def test_random_keep_exact_counts():
 @pytest.mark.parametrize("cc", ["0", "1"])
 def test_cached_group_max_tensor_cores_mismatch_rate_large(n, cc, monkeypatch):
     # up to 32 groups x 4096 keys per head: the fraction of bf16 group-max values that differ from
-    # the NumPy map (printed with -s) stays below 1e-3, each by one bf16 step
+    # the NumPy map (printed with -s) stays below 1e-4, each by one bf16 step
     d, h, m = 128, 2, 128
     monkeypatch.setenv("FGA_CACHED_CC", cc)
     q = oracle.bf16_round(oracle.gaussian((1, h, n, d), 21))
@@ -468,7 +472,7 @@ def test_cached_group_max_tensor_cores_mismatch_rate_large(n, cc, monkeypatch):
     got = gmax.cpu().numpy()
     mism = got != ref
     print(f"cached group max: {mism.mean():.2e} of values differ (n={n}, cc={cc})")
-    assert mism.mean() < 1e-3
+    assert mism.mean() < 1e-4  # measured <= 6.3e-5
     if mism.any():
         rel = np.abs(got[mism] - ref[mism]) / np.maximum(np.abs(ref[mism]), 1e-30)
         assert rel.max() <= 2 ** -7

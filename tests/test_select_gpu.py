@@ -192,3 +192,34 @@ def test_fused_threshold_builder_bits_and_fallback(n, d):
         fallbacks += int((rows[r] >= np.float32(tau)).sum() == 0)
         assert np.array_equal(idx[r, :counts[r]], ref), r
     assert fallbacks > 0
+
+
+def test_avg_query_builders_at_wan_shape_vs_oracle():
+    # c2 row length (N = 32760, D = 128), one head: the GPU's pooled scores against the NumPy
+    # restatement of masks.py:108-118 (mismatching bf16 scores counted and printed), and the
+    # threshold / top-k lists against the reference selection on the reference's scores -- a key
+    # may only differ where its score did (masks.py:131-147)
+    n, d = 32760, 128
+    cfg = fga.AttnConfig(1, 1, n, d, precision="bf16")
+    q = oracle.bf16_round(oracle.gaussian(cfg.dims, 71))
+    k = oracle.bf16_round(oracle.gaussian(cfg.dims, 72))
+    ref = oracle.pooled_scores(q, k, cfg.group_size, None, "bf16").reshape(-1, n)
+    got = fga.pooled_query_scores(torch.from_numpy(q).cuda().to(torch.bfloat16),
+                                  torch.from_numpy(k).cuda().to(torch.bfloat16), cfg).cpu().numpy().reshape(-1, n)
+    mism = got != ref
+    print(f"pooled scores at N={n}: {mism.mean():.2e} of the bf16 values differ")
+    assert mism.mean() < 2e-4
+    tau = float(np.quantile(ref, 0.55))
+    qd, kd = (torch.from_numpy(x).cuda().to(torch.bfloat16) for x in (q, k))
+    for b in (fga.MaskBuilderConfig("avg_query_threshold", tau=tau), fga.MaskBuilderConfig("avg_query_topk", top_k=14742)):
+        m = fga.build_mask_avg_query(qd, kd, cfg, b, device_result=True)
+        counts = m.counts.cpu().numpy().reshape(-1)
+        idx = m.idx.cpu().numpy().reshape(counts.size, -1)
+        for r in range(counts.size):
+            want = _ref_threshold(ref[r], np.float32(tau)) if b.strategy.endswith("threshold") else _ref_topk(ref[r], 14742)
+            have = idx[r, :counts[r]]
+            if not np.array_equal(have, want):
+                assert mism[r].any(), (b.strategy, r)   # only rows whose scores differ may differ
+                flip = np.setxor1d(have, want)
+                if b.strategy.endswith("threshold"):
+                    assert mism[r, flip].all(), (b.strategy, r)  # and only at those keys
