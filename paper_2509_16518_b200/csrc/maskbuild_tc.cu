@@ -39,7 +39,7 @@ namespace fga {
 namespace {
 
 #ifndef FGA_CB_POLY
-#define FGA_CB_POLY 0
+#define FGA_CB_POLY 3
 #endif
 constexpr int CB_POLY = FGA_CB_POLY;  // pass 0: every CB_POLY-th pair of exps on the FMA pipe (0: none)
 constexpr int CB_EW = 4;              // epilogue warps per TMEM lane quadrant
@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
     float* const s32 = p.scores;
     uint32_t* const bits_out = p.keep_bits;
     const uint32_t tau_b16 = __bfloat16_as_ushort(__float2bfloat16_ru(p.tau));  // p.tau > 0
+    const float sl0 = scale * 1.4426950408889634f;  // pass 0: scale * log2e
     (void)rnd; (void)s16; (void)s32; (void)bits_out; (void)tau_b16;
     uint32_t sc = 0;
     for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
         for (int k = 0; k < 32; ++k) nz[k] = -tab[w * 32 + k].z;
       }
       float m = -INFINITY;
+      float ml0 = -INFINITY;  // pass 0: m * log2e
       double den = 0.0;
       for (int c = c_lo; c < c_hi; ++c, ++sc) {
         const uint32_t b = sc % CB_SB;
@@ -337,39 +339,53 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             }
           }
         } else if (PASS == 0) {
-          // columns: keys j = c*128 + 32w + k.  The row max is taken on the raw dot products
-          // (scale > 0 and rounding is monotonic, so fl(max(acc) * scale) = max(fl(acc * scale)),
-          // attention_map's s), and each term exp(s - m) is one FFMA2 + MUFU ex2 on
+          // columns: keys j = c*128 + 32w + k.  Each term exp(s - m) is one FFMA2 + MUFU ex2 on
           // acc * scale * log2e - m * log2e; their rounding errors average out over the row's N
-          // terms, each chunk's 32 summed in fp32, the row in fp64.
+          // terms, each chunk's 32 summed in fp32, the row in fp64.  m is a lazy running max (in
+          // the units of s = fl(acc * scale), attention_map's s): the exps use it until a score
+          // beats it by more than 8 log2 units, which shows up as a chunk sum above 2^8 (all terms
+          // are positive) and sends the warp to the exact path -- the chunk's max on the raw dot
+          // products (scale > 0 and rounding is monotonic, so fl(max(acc) * scale) = max(s)), den
+          // rescaled in fp64, the chunk re-summed.  Pass 1 needs only m + ln den, which any such m
+          // gives exactly; the per-chunk max and the fp64 exp are off the common path.
           const int jbase = c * BN + w * 32;
-          if (jbase + 32 > p.n) {
+          if (jbase + 32 > n_keys) {
 #pragma unroll
             for (int k = 0; k < 32; ++k)
-              if (jbase + k >= p.n) v[k] = __float_as_uint(-INFINITY);
+              if (jbase + k >= n_keys) v[k] = __float_as_uint(-INFINITY);
           }
-          float amax = -INFINITY;
-#pragma unroll
-          for (int k = 0; k < 32; k += 2) amax = fmax3f(amax, __uint_as_float(v[k]), __uint_as_float(v[k + 1]));
-          const float cmax = __fmul_rn(amax, p.scale);
-          if (cmax > m) {
-            den = m == -INFINITY ? 0.0 : den * exp(static_cast<double>(m) - static_cast<double>(cmax));
-            m = cmax;
-          }
-          if (m != -INFINITY) {  // (columns entirely past the sequence end add nothing)
-            const float sl = p.scale * 1.4426950408889634f, ml = m * 1.4426950408889634f;
+          auto chunk_sum = [&](float ml) {
             float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
             for (int k = 0; k < 32; k += 2) {
               const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
-                                          make_float2(sl, sl), make_float2(-ml, -ml));
-              if (CB_POLY > 0 && (k / 2) % CB_POLY == CB_POLY - 1)
+                                          make_float2(sl0, sl0), make_float2(-ml, -ml));
+              if (CB_POLY > 0 && (k / 2) % (CB_POLY > 0 ? CB_POLY : 1) == CB_POLY - 1)
                 acc = __fadd2_rn(acc, ex2_poly2<5>(x));  // this pair on the FMA pipe
               else
                 acc = __fadd2_rn(acc, make_float2(ex2(x.x), ex2(x.y)));
             }
-            den += static_cast<double>(acc.x) + static_cast<double>(acc.y);
+            return acc;
+          };
+          float2 acc = make_float2(0.f, 0.f);
+          bool exact = m == -INFINITY;
+          if (!exact) {
+            acc = chunk_sum(ml0);
+            exact = !(acc.x + acc.y <= 256.f);
           }
+          if (__any_sync(0xffffffffu, exact) && exact) {
+            float amax = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) amax = fmax3f(amax, __uint_as_float(v[k]), __uint_as_float(v[k + 1]));
+            const float cmax = __fmul_rn(amax, scale);
+            if (cmax > m) {
+              den = m == -INFINITY ? 0.0 : den * exp(static_cast<double>(m) - static_cast<double>(cmax));
+              m = cmax;
+              ml0 = m * 1.4426950408889634f;
+            }
+            acc = m == -INFINITY ? make_float2(0.f, 0.f) : chunk_sum(ml0);
+          }
+          if (m != -INFINITY) den += static_cast<double>(acc.x) + static_cast<double>(acc.y);
         } else {
           // columns: the group's queries i = 32w + k; row: key j = c*128 + row.
           float* xy = reinterpret_cast<float*>(smem + L::OFF_XCH) + (sc & 1) * (3 * CB_EW * 128);
