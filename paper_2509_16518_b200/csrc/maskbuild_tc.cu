@@ -45,7 +45,15 @@ constexpr int CB_POLY = FGA_CB_POLY;  // pass 0: every CB_POLY-th pair of exps o
 constexpr int CB_EW = 4;              // epilogue warps per TMEM lane quadrant
 constexpr int CB_EPI = 4 * CB_EW;      // epilogue warps 0..15
 constexpr int CB_WARPS = CB_EPI + 2;   // + MMA issuer + TMA producer
-constexpr int cb_nq(int pass) { return pass == 2 ? 3 : 1; }  // Q-side tiles per unit (pass 2: q̄ hi/mid/lo)
+#ifdef FGA_CB_EXACT_SELECT
+constexpr int CB_P1G = 1;  // pass 1: groups per unit (the exact-select variant keeps one)
+#else
+constexpr int CB_P1G = 2;  // pass 1: two groups per unit share every K chunk (half the L2 -> SMEM bytes)
+#endif
+// Q-side tiles per unit: pass 2 q̄ hi/mid/lo (accumulated into one score tile), pass 1 the unit's
+// CB_P1G groups (one score tile each), pass 0 one query tile
+constexpr int cb_nq(int pass) { return pass == 2 ? 3 : pass == 1 ? CB_P1G : 1; }
+constexpr int cb_sbw(int pass) { return pass == 1 ? 128 * CB_P1G : 128; }  // TMEM columns per S buffer
 constexpr int cb_ns(int pass) { return pass == 2 ? 3 : 4; }  // K ring slots
 constexpr int CB_NS = 4;                                      // barrier slots (max ring)
 constexpr int CB_SB = 4;  // S buffers in TMEM (4 x 128 columns): the MMA runs up to 3 tiles ahead
@@ -55,11 +63,13 @@ template <int D, int PASS>
 struct CbSmem {
   static constexpr int KV = (D / 64) * HALF;  // one 128-row tile
   static constexpr int NQ = cb_nq(PASS), NS = cb_ns(PASS);
+  static constexpr int SBW = cb_sbw(PASS), NSB = 128 * CB_SB / SBW;  // S buffer width / count in TMEM
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = NQ * KV;
   static constexpr int OFF_BAR = OFF_K + NS * KV;
   static constexpr int OFF_TAB = OFF_BAR + 256;       // pass 1: (m_i, 1/den_i, m_i + ln den_i) per query
-  static constexpr int OFF_XCH = OFF_TAB + 128 * 16;  // pass 0: (m, den) per slice; pass 1: candidates x 2
+  static constexpr int OFF_NZ = OFF_TAB + CB_P1G * 128 * 16;  // pass 1: -(m_i + ln den_i) of the unit's groups
+  static constexpr int OFF_XCH = OFF_NZ + CB_P1G * 128 * 4;     // pass 0: (m, den) per slice; pass 1: candidates x 2
   static constexpr int BYTES = OFF_XCH + 2 * 3 * CB_EW * 128 * 4;
   static_assert(CB_EW * 128 * 12 <= 2 * 3 * CB_EW * 128 * 4, "exchange area");
   static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
@@ -88,7 +98,7 @@ __device__ __forceinline__ CbBars cb_bars(uint8_t* smem) {
 struct CbParams {
   int64_t bh;   // B * H
   int n;        // sequence length
-  int tiles;    // units per (b, h): ceil(n / 128) query tiles = groups (passes 0, 1), ceil(G / 128) group tiles (pass 2)
+  int tiles;    // units per (b, h): ceil(n / 128) query tiles (pass 0), ceil(G / CB_P1G) group pairs (pass 1), ceil(G / 128) group tiles (pass 2)
   int nch;      // key chunks per unit: ceil(n / 128)
   int groups;   // pass 2: G
   int64_t part_rows;  // pass 2: rows of one q̄ part (B*H*G)
@@ -169,7 +179,8 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
         mbar_expect_tx(bar.q_full, L::NQ * BM * D * 2);
 #pragma unroll
         for (int qp = 0; qp < L::NQ; ++qp) {
-          const int qrow = PASS == 2 ? static_cast<int>(qp * p.part_rows + bh * p.groups) + t * BM : row0 + t * BM;
+          const int qrow = PASS == 2 ? static_cast<int>(qp * p.part_rows + bh * p.groups) + t * BM
+                                     : row0 + (t * L::NQ + qp) * BM;  // pass 1: group CB_P1G*t + qp
 #pragma unroll
           for (int h = 0; h < D / 64; ++h)
             tma_load_2d(smem + L::OFF_Q + qp * L::KV + h * HALF, &tmQ, bar.q_full, h * 64, qrow, pol_q);
@@ -198,9 +209,9 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       unit(u, bh, t, c_lo, c_hi);
       mbar_wait(bar.q_full, it & 1);
       for (int c = c_lo; c < c_hi; ++c, ++kc, ++sc) {
-        const uint32_t slot = kc % L::NS, use = kc / L::NS, b = sc % CB_SB;
+        const uint32_t slot = kc % L::NS, use = kc / L::NS, b = sc % L::NSB;
         mbar_wait(&bar.k_full[slot], use & 1);
-        mbar_wait(&bar.s_empty[b], ((sc / CB_SB) & 1) ^ 1);
+        mbar_wait(&bar.s_empty[b], ((sc / L::NSB) & 1) ^ 1);
         tc_fence_after();
         const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
         if (elect_one()) {
@@ -210,9 +221,10 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             for (int kk = 0; kk < D / 16; ++kk) {
               const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
               const uint64_t dq = dq0 + ((qp * L::KV) >> 4) + off;
-              const uint32_t acc = (qp > 0 || kk > 0) ? 1u : 0u;
-              if (PASS == 0) umma_ss(tmem + b * 128, dq, dk + off, IDESC, acc);  // S = Q K^T
-              else umma_ss(tmem + b * 128, dk + off, dq, IDESC, acc);            // S^T = K Q^T
+              if (PASS == 0) umma_ss(tmem + b * L::SBW, dq, dk + off, IDESC, kk > 0 ? 1u : 0u);  // S = Q K^T
+              else if (PASS == 1)  // S^T = K Q_g^T, one 128-column tile per group of the unit
+                umma_ss(tmem + b * L::SBW + qp * 128, dk + off, dq, IDESC, kk > 0 ? 1u : 0u);
+              else umma_ss(tmem + b * L::SBW, dk + off, dq, IDESC, (qp > 0 || kk > 0) ? 1u : 0u);
             }
           }
           umma_commit(&bar.s_full[b]);
@@ -244,10 +256,10 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       int t, c_lo, c_hi;
       unit(u, bh, t, c_lo, c_hi);
       const int64_t row0 = bh * p.n;
-      const int q0 = t * BM;
+      const int q0 = t * L::NQ * BM;  // pass 1: the first query of the unit's first group
       if (PASS == 1) {
-        // the group's (m_i, 1/den_i, m_i + ln den_i); rows past the sequence end are never selected
-        if (tid < 128) {
+        // the groups' (m_i, 1/den_i, m_i + ln den_i); rows past the sequence end are never selected
+        if (tid < L::NQ * 128) {
           const int i = q0 + tid;
           float4 e = make_float4(0.f, 0.f, INFINITY, 0.f);
           if (i < p.n) {
@@ -255,27 +267,30 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             e = make_float4(mi, ri, mi - logf(ri), 0.f);
           }
           reinterpret_cast<float4*>(smem + L::OFF_TAB)[tid] = e;
+          reinterpret_cast<float*>(smem + L::OFF_NZ)[tid] = -e.z;
         }
         epi_bar();
       }
-      float nz[32];  // pass 1: -(m_i + ln den_i) of this warp's 32 queries, in registers for the unit
-      if (PASS == 1) {
+      float nz[1][32];  // pass 1: -(m_i + ln den_i) of this warp's 32 queries of the unit's first group
+      if (PASS == 1) {  // (the second group's are read from shared memory per chunk: registers)
 #pragma unroll
-        for (int k = 0; k < 32; ++k) nz[k] = -tab[w * 32 + k].z;
+        for (int k = 0; k < 32; ++k) nz[0][k] = -tab[w * 32 + k].z;
       }
       float m = -INFINITY;
       float ml0 = -INFINITY;  // pass 0: m * log2e
       double den = 0.0;
       for (int c = c_lo; c < c_hi; ++c, ++sc) {
-        const uint32_t b = sc % CB_SB;
-        mbar_wait(&bar.s_full[b], (sc / CB_SB) & 1);
+        const uint32_t b = sc % L::NSB;
+        mbar_wait(&bar.s_full[b], (sc / L::NSB) & 1);
         tc_fence_after();
         uint32_t v[32];
-        tmem_ld32(tl + b * 128, v);
+        tmem_ld32(tl + b * L::SBW, v);
         tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar.s_empty[b]);
+        if (PASS != 1 || CB_P1G == 1) {  // (pass 1 reads its second group's tile first)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar.s_empty[b]);
+        }
         if (PASS == 2) {
           // row: key j = c*128 + row; columns: groups g = 128t + 32w + k (masks.py:108-118):
           // s = exp(k_j . q̄_g * scale) / D, bf16-rounded
@@ -390,20 +405,52 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
           // columns: the group's queries i = 32w + k; row: key j = c*128 + row.
           float* xy = reinterpret_cast<float*>(smem + L::OFF_XCH) + (sc & 1) * (3 * CB_EW * 128);
 #ifndef FGA_CB_EXACT_SELECT
-          // y_j = max_i s_ij - (m_i + ln den_i); gmax_gj = exp(y_j)
-          float by = -INFINITY;
+          // y_j = max_i s_ij - (m_i + ln den_i); gmax_gj = exp(y_j), for each group of the unit
+          auto col_max = [&](const float (&nzg)[32]) {
+            float y = -INFINITY;
 #pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            const float2 y2 = __ffma2_rn(make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
-                                         make_float2(p.scale, p.scale), make_float2(nz[k], nz[k + 1]));
-            by = fmax3f(by, y2.x, y2.y);
+            for (int k = 0; k < 32; k += 2) {
+              const float2 y2 = __ffma2_rn(make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                                           make_float2(scale, scale), make_float2(nzg[k], nzg[k + 1]));
+              y = fmax3f(y, y2.x, y2.y);
+            }
+            return y;
+          };
+          float by[CB_P1G];
+          by[0] = col_max(nz[0]);
+          if (CB_P1G == 2) {  // the second group's tile, then the buffer goes back to the MMA
+            tmem_ld32(tl + b * L::SBW + 128, v);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar.s_empty[b]);
+            float nz1[32];
+            const float4* nzs = reinterpret_cast<const float4*>(smem + L::OFF_NZ + (128 + w * 32) * 4);
+#pragma unroll
+            for (int k4 = 0; k4 < 8; ++k4) {
+              const float4 z = nzs[k4];
+              nz1[4 * k4] = z.x; nz1[4 * k4 + 1] = z.y; nz1[4 * k4 + 2] = z.z; nz1[4 * k4 + 3] = z.w;
+            }
+            by[CB_P1G - 1] = col_max(nz1);
           }
-          if (w > 0) xy[w * 128 + row] = by;
+          if (w > 0) {
+#pragma unroll
+            for (int gi = 0; gi < CB_P1G; ++gi) xy[(gi * CB_EW + w) * 128 + row] = by[gi];
+          }
           epi_bar();  // double-buffered by chunk parity: one barrier per chunk
           if (w == 0) {
+            const int j = c * BN + row;
 #pragma unroll
-            for (int o = 1; o < CB_EW; ++o) by = fmaxf(by, xy[o * 128 + row]);
-            float g = expf(by);
+            for (int gi = 0; gi < CB_P1G; ++gi) {
+              float y = by[gi];
+#pragma unroll
+              for (int o = 1; o < CB_EW; ++o) y = fmaxf(y, xy[(gi * CB_EW + o) * 128 + row]);
+              float g = expf(y);
+              if (p.round) g = __bfloat162float(__float2bfloat16_rn(g));
+              const int grp = t * CB_P1G + gi;
+              if (j < p.n && grp < p.groups) p.gmax[(bh * p.groups + grp) * static_cast<int64_t>(p.n) + j] = g;
+            }
+          }
 #else
           // select the query maximising s_ij - (m_i + ln den_i), then evaluate
           // a_ij = expf(s_ij - m_i) / den_i as the reference does for that one query
@@ -411,7 +458,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
           int bi = 0;
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            const float y = fmaf(__uint_as_float(v[k]), p.scale, nz[k]);
+            const float y = fmaf(__uint_as_float(v[k]), p.scale, nz[0][k]);
             if (y > by) {
               by = y;
               bacc = __uint_as_float(v[k]);
@@ -436,11 +483,11 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             }
             const float4 e = tab[bi];
             float g = __fmul_rn(expf(__fsub_rn(__fmul_rn(bacc, p.scale), e.x)), e.y);
-#endif
             if (p.round) g = __bfloat162float(__float2bfloat16_rn(g));
             const int j = c * BN + row;
-            if (j < p.n) p.gmax[(bh * p.tiles + t) * static_cast<int64_t>(p.n) + j] = g;
+            if (j < p.n) p.gmax[(bh * p.groups + t) * static_cast<int64_t>(p.n) + j] = g;
           }
+#endif
         }
       }
       if (PASS == 0) {
@@ -516,8 +563,13 @@ int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s,
   p.row_max = row_max;
   p.row_rinv = rinv;
   p.gmax = gmax;
+  p.groups = p.tiles;  // M = 128: one query tile per group
   rc = D == 64 ? launch_pass<64, 0>(maps, p, st) : launch_pass<128, 0>(maps, p, st);
-  if (rc == FGA_OK) rc = D == 64 ? launch_pass<64, 1>(maps, p, st) : launch_pass<128, 1>(maps, p, st);
+  if (rc == FGA_OK) {
+    CbParams p1 = p;
+    p1.tiles = (p.groups + CB_P1G - 1) / CB_P1G;  // units per (b, h): CB_P1G groups each
+    rc = D == 64 ? launch_pass<64, 1>(maps, p1, st) : launch_pass<128, 1>(maps, p1, st);
+  }
   return rc;
 }
 
