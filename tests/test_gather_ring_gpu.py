@@ -5,7 +5,6 @@ gather_rows (/root/reference/pkg/src/sliceattn/sparse.py:95-108) bitwise, with t
 last chunk zero-filled -- the rows the tensor core reads for S = Q K^T and O += P V.
 GPU only."""
 
-import numpy as np
 import pytest
 
 from conftest import cuda_ok
