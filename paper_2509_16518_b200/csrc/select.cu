@@ -43,10 +43,9 @@ __device__ __forceinline__ uint32_t okey_bits(uint32_t k) {  // inverse of okey2
 }
 __device__ __forceinline__ float bf16_value(uint32_t b) { return __uint_as_float(b << 16); }
 
-// sum over the block of one int per thread; `red` holds two buffers of SEL_WARPS (the phase
-// alternates, so one barrier per call suffices)
+// sum over the block of the warps' partial sums (v: this warp's, the same in every lane); `red`
+// holds two buffers of SEL_WARPS (the phase alternates, so one barrier per call suffices)
 __device__ __forceinline__ int block_sum(int v, int* red, int& phase) {
-  v = __reduce_add_sync(0xffffffffu, v);
   int* r = red + phase * SEL_WARPS;
   if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
   __syncthreads();
@@ -117,6 +116,12 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
   int phase = 0;
   float thr = 0.f;  // top-k: the k-th largest value
   int need = 0;
+  // warp w owns the contiguous 256-key blocks [b0, b1) (lane l: keys 8l..8l+7 of each) in every
+  // pass below, so the bisection's per-warp counts double as the emission's per-warp counts
+  const int nb = (nv + 31) / 32;
+  const int bpw = (nb + SEL_WARPS - 1) / SEL_WARPS;
+  const int b0 = min(nb, warp * bpw), b1 = min(nb, b0 + bpw);
+  int warp_ge = 0, warp_gt = 0;  // top-k: this warp's #{s >= thr}, #{s > thr}
   if (TOPK) {
     // ---- 2. bisection over the order-preserving keys: thr = max { v : #{s >= value(v)} >= k },
     //      #{s >= value(kmin)} = n >= k.  Each pass counts with HSET2.BF16 (a 0xFFFF mask per
@@ -134,39 +139,52 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
     }
     __syncthreads();  // s_red is reused by block_sum
     const int k = static_cast<int>(top_k);
-    while (lo < hi) {  // block-uniform
-      const uint32_t mid = (lo + hi + 1) >> 1, pb = okey_bits(mid) * 0x00010001u;
+    // this warp's #{s >= value(v)}
+    auto count_ge = [&](uint32_t v) {
+      const uint32_t pb = okey_bits(v) * 0x00010001u;
       const __nv_bfloat162 piv = *reinterpret_cast<const __nv_bfloat162*>(&pb);
       uint32_t acc = 0;  // two 16-bit counters of -1s (|count| <= n/16 per thread each)
-      for (int i = tid; i < nv; i += SEL_THREADS) {
-        const uint4 x = sv[i];
-        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.x), piv));
-        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.y), piv));
-        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.z), piv));
-        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.w), piv));
+      for (int b = b0; b < b1; ++b) {
+        const int vi = b * 32 + lane;
+        if (vi < nv) {
+          const uint4 x = sv[vi];
+          acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.x), piv));
+          acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.y), piv));
+          acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.z), piv));
+          acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.w), piv));
+        }
       }
       const int mine = static_cast<int>(((0x10000u - (acc & 0xFFFFu)) & 0xFFFFu) + ((0x10000u - (acc >> 16)) & 0xFFFFu));
-      const int c = block_sum(mine, s_red, phase);
-      if (c >= k) lo = mid; else hi = mid - 1;
+      return __reduce_add_sync(0xffffffffu, mine);
+    };
+    // invariant: #{s >= value(lo)} >= k, #{s >= value(hi + 1)} < k; each pass's per-warp count is
+    // kept for the side it moves, so at the end #{s >= thr} and #{s > thr} = #{s >= value(thr + 1)}
+    // are known per warp without another pass (consecutive keys are consecutive bf16 values apart
+    // from -0 / +0, which can never straddle the final interval)
+    bool have_lo = false;
+    while (lo < hi) {  // block-uniform
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      const int wc = count_ge(mid);
+      const int c = block_sum(wc, s_red, phase);
+      if (c >= k) { lo = mid; warp_ge = wc; have_lo = true; }
+      else { hi = mid - 1; warp_gt = wc; }
     }
+    if (!have_lo) warp_ge = count_ge(lo);  // the k-th value is the row's minimum
     thr = bf16_value(okey_bits(lo));
     need = k;  // minus the keys above thr: the ties at thr kept in index order
   } else {
     __syncthreads();
   }
 
-  // ---- 3. per-warp counts over contiguous ranges of 256-key blocks (lane l: keys 8l..8l+7)
-  //      top-k: keys above thr and ties at thr; threshold: keys >= tau (a bf16 compare against
-  //      tau rounded up to bf16 is exact).  Masks accumulated 16x2 as in the bisection.
-  const uint32_t cut = TOPK ? __bfloat16_as_ushort(__float2bfloat16_rn(thr))
-                            : __bfloat16_as_ushort(__float2bfloat16_ru(tau));
-  const uint32_t cut2b = cut * 0x00010001u;
-  const __nv_bfloat162 cut2 = *reinterpret_cast<const __nv_bfloat162*>(&cut2b);
-  const int nb = (nv + 31) / 32;
-  const int bpw = (nb + SEL_WARPS - 1) / SEL_WARPS;
-  const int b0 = min(nb, warp * bpw), b1 = min(nb, b0 + bpw);
-  {
-    uint32_t ga = 0, ea = 0;
+  // ---- 3. per-warp counts: top-k from the bisection (keys above thr, ties at thr); threshold:
+  //      keys >= tau over the warp's blocks (a bf16 compare against tau rounded up to bf16 is
+  //      exact), masks accumulated 16x2 as in the bisection
+  if (TOPK) {
+    if (lane == 0) { s_cnt[0][warp] = warp_gt; s_cnt[1][warp] = warp_ge - warp_gt; }
+  } else {
+    const uint32_t cut2b = __bfloat16_as_ushort(__float2bfloat16_ru(tau)) * 0x00010001u;
+    const __nv_bfloat162 cut2 = *reinterpret_cast<const __nv_bfloat162*>(&cut2b);
+    uint32_t ga = 0;
     for (int b = b0; b < b1; ++b) {
       const int vi = b * 32 + lane;
       if (vi < nv) {
@@ -175,19 +193,13 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
-          if (TOPK) {
-            ga = __vadd2(ga, __hgt2_mask(h, cut2));
-            ea = __vadd2(ea, __heq2_mask(h, cut2));
-          } else {
-            ga = __vadd2(ga, __hge2_mask(h, cut2));
-          }
+          ga = __vadd2(ga, __hge2_mask(h, cut2));
         }
       }
     }
     const int g = static_cast<int>(((0x10000u - (ga & 0xFFFFu)) & 0xFFFFu) + ((0x10000u - (ga >> 16)) & 0xFFFFu));
-    const int e = static_cast<int>(((0x10000u - (ea & 0xFFFFu)) & 0xFFFFu) + ((0x10000u - (ea >> 16)) & 0xFFFFu));
-    const int gs = __reduce_add_sync(0xffffffffu, g), es = __reduce_add_sync(0xffffffffu, e);
-    if (lane == 0) { s_cnt[0][warp] = gs; s_cnt[1][warp] = es; }
+    const int gs = __reduce_add_sync(0xffffffffu, g);
+    if (lane == 0) { s_cnt[0][warp] = gs; s_cnt[1][warp] = 0; }
   }
   __syncthreads();
   int total_gt = 0, base = 0, eqrun = 0;
