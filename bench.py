@@ -741,6 +741,22 @@ def extras(args, torch, np, fga, cfg, q, k, v, keep, mask, out, kernel_ms, flush
     heads, n, d, m = cfg.heads, cfg.seq_len, cfg.head_dim, cfg.group_size
     if out is None:
         out = fga.sparse_attention(q, k, v, mask, cfg)
+    # ---- sustained: the same launch back to back for ~1 s (no L2 flush, the board at its power
+    #      cap), next to the burst number of the timed steps
+    n_sus = max(20, int(1000.0 / max(kernel_ms, 0.05)))
+    fga.sparse_attention(q, k, v, mask, cfg)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(q.device.index) as clk_sus:
+        ev0.record(stream)
+        for _ in range(n_sus):
+            fga.sparse_attention(q, k, v, mask, cfg)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    sus_ms = ev0.elapsed_time(ev1) / n_sus
+    line["sustained"] = {"launches": n_sus, "ms_per_launch": sus_ms,
+                         "tflops": line["roofline"]["achieved"] * kernel_ms / sus_ms if "roofline" in line else None,
+                         "clocks": clk_sus.summary(), "l2": "not flushed (back to back)"}
     # ---- dense denominators on the same GPU and shard: our dense kernel + torch SDPA backends
     dense = {}
     t_own = timed_steps(torch, lambda: fga.flash_attention(q, k, v, cfg), max(3, args.steps // 2), flush, stream)
