@@ -177,7 +177,6 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
         const uint32_t step = static_cast<uint32_t>(static_cast<uint64_t>(c_lo - k) * span / static_cast<uint64_t>(c_lo - c_hi1));
         mid = lo + min(max(step, 1u), hi - lo);
       }
-      const uint32_t before = hi - lo;
       const int wc = count_ge(mid);
       const int c = block_sum(wc, s_red, phase);
       if (c >= k) { lo = mid; warp_ge = wc; have_lo = true; c_lo = c; }
@@ -185,7 +184,6 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
       // alternate (interpolating again whenever the last step halved the interval measured slower:
       // 241.7 vs 229.4 us at c2, the one-sided regula-falsi steps)
       interp = FGA_SEL_INTERP != 0 && !interp;
-      (void)before;
     }
     if (!have_lo) warp_ge = count_ge(lo);  // the k-th value is the row's minimum
     thr = bf16_value(okey_bits(lo));
