@@ -16,10 +16,12 @@
 //
 // One 512-thread CTA per (b,h,g) row:
 //   1. load: global bf16 -> SMEM (+ min / max of the order-preserving 16-bit keys),
-//   2. top-k: thr = the largest value v with #{s >= v} >= k (bisection over [min, max] keys),
-//   3. count: warp w owns a contiguous range of 32-key words and counts its kept keys
-//      (> thr, == thr) with ballots; one block scan gives every warp its output offset and the
-//      number of threshold ties before its range (ties are kept in index order until k),
+//   2. top-k: thr = the largest value v with #{s >= v} >= k (interpolation steps alternating
+//      with bisection steps over [min, max] keys),
+//   3. count: warp w owns a contiguous range of 256-key blocks; its kept keys (> thr, == thr) are
+//      the bisection's last per-warp counts (threshold: one counting pass); one block scan gives
+//      every warp its output offset and the number of threshold ties before its range (ties are
+//      kept in index order until k),
 //   4. emit: each warp writes its kept positions in order (ballot ranks, coalesced stores).
 // Output bit-exact with the reference lists for the same bf16 scores.  HBM-bound: 2n bytes read
 // and 4*count (+ the -1 tail) written per row.
