@@ -59,6 +59,40 @@ def test_cabi_validation_without_gpu():
         _lib.check(rc, "x")
 
 
+def test_workspace_sizes_without_gpu():
+    # the library never allocates: every scratch buffer is sized by fga_workspace_bytes (host-only)
+    shp = _lib.shape(1, 12, 32760, 128, 128)
+    g = 256
+    pooled = _lib.workspace_bytes(_lib.FGA_WS_POOLED_SCORES, shp)
+    assert pooled >= 12 * g * 128 * 4 + 3 * 12 * g * 128 * 2           # q-bar fp32 + its 3 bf16 parts
+    assert _lib.workspace_bytes(_lib.FGA_WS_CACHED_GROUP_MAX, shp) >= 12 * 32760 * (4 + 8)
+    cells = 12 * g * 32760
+    assert _lib.workspace_bytes(_lib.FGA_WS_BUILD_AVGQ, shp, 1) >= pooled + 2 * cells   # bf16 scores
+    assert _lib.workspace_bytes(_lib.FGA_WS_BUILD_AVGQ, shp, 0) >= pooled + 5 * cells   # fp32 + keep bytes
+    assert _lib.workspace_bytes(_lib.FGA_WS_BUILD_CACHED, shp) >= 5 * cells
+    assert _lib.load().fga_workspace_bytes(99, shp, 1) == _lib.FGA_EINVAL
+    assert _lib.load().fga_workspace_bytes(1, _lib.shape(1, 1, 10, 64, 20), 1) == _lib.FGA_EINVAL
+
+
+def test_builder_and_select_argument_checks_without_gpu():
+    # the reference's ValueErrors (masks.py:100-101, :139-140) and shape checks, before any launch
+    lib = _lib.load()
+    shp = _lib.shape(1, 1, 256, 64, 128)
+    args = lambda strategy, tau, k, stride=256: (1, 1, shp, strategy, tau, k, 1, 1, stride, 1, 0, None, 0, None)
+    assert lib.fga_build_mask_avgq(*args(_lib.FGA_SELECT_THRESHOLD, 0.0, 1)) == _lib.FGA_EINVAL  # tau <= 0
+    assert b"tau" in lib.fga_last_error()
+    assert lib.fga_build_mask_avgq(*args(_lib.FGA_SELECT_TOPK, 0.0, 257)) == _lib.FGA_EINVAL     # top_k > N
+    assert lib.fga_build_mask_avgq(*args(7, 1.0, 1)) == _lib.FGA_EINVAL                          # strategy
+    assert lib.fga_build_mask_avgq(*args(_lib.FGA_SELECT_TOPK, 0.0, 5, stride=100)) == _lib.FGA_EINVAL
+    assert lib.fga_build_mask_cached(1, 1, shp, -1.0, 1, 1, 256, 1, 0, None, 0, None) == _lib.FGA_EINVAL
+    assert lib.fga_select_compact(1, 2, 100, _lib.FGA_SELECT_TOPK, 0.0, 0, 1, 100, 1, 0, None) == _lib.FGA_EINVAL
+    big = _lib.FGA_SELECT_MAX_N + 1
+    assert lib.fga_select_compact(1, 2, big, _lib.FGA_SELECT_TOPK, 0.0, 1, 1, big, 1, 0, None) == _lib.FGA_EUNSUPPORTED
+    # workspace alignment is checked before any launch
+    assert lib.fga_pooled_scores(1, 1, shp, 1, 1, 8, 1 << 20, None) == _lib.FGA_EINVAL
+    assert b"aligned" in lib.fga_last_error()
+
+
 def test_product_path_has_no_cpu_fallback():
     try:
         import torch
