@@ -306,3 +306,30 @@ def test_full_mask_dispatches_to_the_dense_kernel(n, m, monkeypatch):
                                   out_dtype=torch.float32)
     assert not torch.equal(o_part[0, 1, :m], o_dense[0, 1, :m])  # ran the gather kernel, one key short
     assert (o_part[0, 0] - o_dense[0, 0]).abs().max().item() <= (1e-5 if m <= 128 else ATOL)
+
+
+def test_sparse_attention_replays_in_a_cuda_graph():
+    # the device path is stream-ordered with no host sync after a mask's first use (its tile order
+    # and full-mask check are cached), so a launch-bound call can be captured once and replayed:
+    # bitwise the eager result, with inputs updated in place between replays
+    cfg = fga.AttnConfig(1, 2, 4096, 64, precision="bf16")
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn(cfg.dims, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    mask = fga.random_mask_device(cfg, 0.3, seed=1)
+    eager = fga.sparse_attention(q, k, v, mask, cfg)      # first use: validation, tile order cached
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fga.sparse_attention(q, k, v, mask, cfg)
+    torch.cuda.current_stream().wait_stream(side)
+    with torch.cuda.graph(graph):
+        out = fga.sparse_attention(q, k, v, mask, cfg)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+    q.copy_(torch.randn(cfg.dims, device="cuda", generator=g).to(torch.bfloat16))
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, fga.sparse_attention(q, k, v, mask, cfg))
