@@ -288,9 +288,16 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
     } else {
       base += tot & 0xFFFF;
     }
+    // a running output pointer stepped by the keep bit: predicated stores, no per-slot address
+    // arithmetic or branch
+    int32_t* op = out + at;
+    const int key0 = vi * 8;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (keep & (1u << j)) out[at++] = vi * 8 + j;
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t kj = (keep >> j) & 1u;
+      if (kj) *op = key0 + j;
+      op += kj;
+    }
   }
 
   if (!TOPK && total == 0) {
