@@ -687,8 +687,12 @@ def ours(args):
         if rank == 0:
             line["e2e"] = e2e
         if rank == 0:
-            extras(args, torch, np, fga, lcfg, lq, lk, lv, lkeep, lmask, out if world == 1 else None, my_ms,
-                   flush, stream, line, world, hbm_peak, peak_src, count)
+            try:  # rank-0-only legs (no collectives): a failure there must not lose the contract line
+                extras(args, torch, np, fga, lcfg, lq, lk, lv, lkeep, lmask, out if world == 1 else None, my_ms,
+                       flush, stream, line, world, hbm_peak, peak_src, count)
+            except Exception as exc:  # noqa: BLE001
+                line["extras_error"] = f"{type(exc).__name__}: {exc}"
+                torch.cuda.synchronize()
         sweep = args.sweep == "on" or (args.sweep is None and world == 8 and mode == "heads")
         if sweep:
             res = c5_sweep(args, torch, fga, _lib, shard, dist, dev, flush, stream, world, rank)
