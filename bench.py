@@ -692,7 +692,6 @@ def ours(args):
                        flush, stream, line, world, hbm_peak, peak_src, count)
             except Exception as exc:  # noqa: BLE001
                 line["extras_error"] = f"{type(exc).__name__}: {exc}"
-                torch.cuda.synchronize()
         sweep = args.sweep == "on" or (args.sweep is None and world == 8 and mode == "heads")
         if sweep:
             res = c5_sweep(args, torch, fga, _lib, shard, dist, dev, flush, stream, world, rank)
