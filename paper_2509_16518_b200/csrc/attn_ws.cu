@@ -50,18 +50,14 @@
 namespace fga {
 namespace {
 
-#ifndef FGA_WS2
-#define FGA_WS2 0  // experiment: two softmax groups of 8 warps on alternating chunks (see softmax2)
-#endif
-constexpr int NSOFT = FGA_WS2 ? 16 : 8;       // softmax warps
-constexpr int PGRP = FGA_WS2 ? 8 : NSOFT;      // softmax warps per S/P buffer (p_full count)
-constexpr int WARP_MMA0 = NSOFT;               // MMA issuers (buffer 0, buffer 1)
-constexpr int WARP_PROD0 = NSOFT + 2;
-constexpr int NPROD = 4;      // gather producers
-constexpr int WARP_SCHED = NSOFT + 6;
+constexpr int NSOFT = 8;      // softmax warps
+constexpr int WARP_MMA0 = 8;  // MMA issuers 8 (buffer 0) and 9 (buffer 1)
+constexpr int WARP_PROD0 = 10;
+constexpr int NPROD = 4;      // gather producers 10-13
+constexpr int WARP_SCHED = 14;
 constexpr int NSCHED = 16;    // tile ring entries
 constexpr int NCONSUMERS = NSOFT + 2 + NPROD;  // warps that read every tile ring entry
-constexpr int NWARPS = FGA_WS2 ? 24 : 16;
+constexpr int NWARPS = 16;
 constexpr int REG_SOFTMAX = 184;
 constexpr int REG_OTHER = 72;  // producers and issuers: measured 13% slower at 64
 #ifndef FGA_NSK
@@ -99,7 +95,7 @@ struct WsSmem {
   static constexpr int OFF_BAR = OFF_V + NSV * KV;
   static constexpr int NBAR = 2 * (NSK + NSV) + 2 + 2 + 2 + 3 + 1 + 2 * NSCHED;
   static constexpr int OFF_XCH = OFF_BAR + ((NBAR * 8 + 16 + 15) / 16) * 16;  // epilogue: m, l per row
-  static constexpr int OFF_SCHED = OFF_XCH + 4 * 128 * 4;                      // tile ring: int64 ids
+  static constexpr int OFF_SCHED = OFF_XCH + 2 * 128 * 4;                      // tile ring: int64 ids
   static constexpr int BYTES = OFF_SCHED + NSCHED * 8;
   static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
   static_assert(WARP_PROD0 + NPROD <= NWARPS, "too many producer warps");
@@ -375,7 +371,7 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
 }
 
 // ------------------------------------------------------------------ softmax warps
-__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * NSOFT) : "memory"); }
+__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // Q rows of tile t -> TMEM (A operand of S = Q K^T): warp (q, h) writes lanes
 // 32q..32q+31 (thread = row), packed bf16 columns [h*D/4, (h+1)*D/4).
@@ -622,201 +618,6 @@ __device__ __forceinline__ void softmax(const AttnParams& p, const void* qptr, c
   }
 }
 
-#if FGA_WS2
-// Experiment: two softmax groups (warps 0-7 and 8-15), group g exponentiating the chunks of
-// CTA-wide parity g (S buffer g), so each group has two chunk periods per chunk.  Both groups
-// must use the same max for a row (one O accumulator): the group that owns the tile's first
-// chunk takes that chunk's exact row max as the tile's fixed max and hands it to the other group
-// through shared memory (named barrier 2).  No rescaling: P = 2^(s - m) may exceed 1 (bf16/fp32
-// keep the relative precision); a chunk row sum above 2^64 sets status bit 16 (prototype).
-// The chunk is processed in two 64-column halves (32 score registers), so every warp fits the
-// 80 registers of a 768-thread CTA without setmaxnreg.
-template <int D>
-__device__ __forceinline__ void exp_half(const uint32_t (&sv)[32], float sl2, const float (&m_use)[2],
-                                         uint32_t (&pk)[16], float2 (&sum2)[2][2]) {
-  const float2 sc2 = make_float2(sl2, sl2);
-  const float2 nm[2] = {make_float2(-m_use[0], -m_use[0]), make_float2(-m_use[1], -m_use[1])};
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const float2 sx = make_float2(__uint_as_float(sv[4 * k + 2 * r]), __uint_as_float(sv[4 * k + 2 * r + 1]));
-      const float2 x = __ffma2_rn(sx, sc2, nm[r]);
-      const float2 pr = make_float2(ex2(x.x), ex2(x.y));
-      sum2[r][k & 1] = __fadd2_rn(sum2[r][k & 1], pr);
-      pk[2 * k + r] = pack_bf16(pr.x, pr.y);
-    }
-  }
-}
-
-__device__ __forceinline__ void mask_half(uint32_t (&sv)[32], int col0, int nvalid, int a) {
-#pragma unroll
-  for (int k = 0; k < 8; ++k)
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-      if (col0 + 8 * k + 2 * a + e >= nvalid) {
-        sv[4 * k + e] = __float_as_uint(-INFINITY);
-        sv[4 * k + 2 + e] = __float_as_uint(-INFINITY);
-      }
-}
-
-template <int D, bool OUT_F32>
-__device__ __forceinline__ void softmax2(const AttnParams& p, const void* qptr, const Bars& bar, uint32_t tmem, int tid,
-                                         float* xch) {
-  const int warp = tid >> 5, lane = tid & 31;
-  const int g = warp >> 3, q = warp & 3, h = (warp >> 2) & 1, a = lane & 3, b = lane >> 2;
-  const int part = warp >> 2;  // epilogue / Q: quarter of the columns
-  const uint32_t lanes16 = static_cast<uint32_t>(q * 32 + h * 16) << 16;
-  const int r0 = q * 32 + h * 16 + b;
-  const float sl2 = p.scale_log2;
-  float* xm = xch;  // [128] the tile's fixed row max, owner group -> other group
-  uint32_t chunk = 0;
-  int it = 0;
-  constexpr int NOC = D / 4;  // O columns per warp in the epilogue
-  constexpr int NQC = D / 8;  // packed Q columns per warp
-  const uint32_t tOw = tmem + TM_O + (static_cast<uint32_t>(q * 32) << 16) + part * NOC;
-  auto put_q = [&](const Tile& t) {
-    const int row = q * 32 + lane;
-    const bool ok = row < t.rows;
-    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(qptr) +
-                                                      (static_cast<int64_t>(t.row0) + t.q0 + row) * D + part * (D / 4));
-    uint32_t v[NQC];
-#pragma unroll
-    for (int i = 0; i < NQC / 4; ++i) {
-      const uint4 x = ok ? __ldg(src + i) : make_uint4(0u, 0u, 0u, 0u);
-      v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
-    }
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + TM_Q + part * NQC;
-    if constexpr (NQC == 16) tmem_st16(taddr, v); else tmem_st8(taddr, v);
-  };
-  auto zero_o = [&]() {
-    uint32_t z[NOC];
-#pragma unroll
-    for (int i = 0; i < NOC; ++i) z[i] = 0u;
-    if constexpr (NOC == 32) tmem_st32(tOw, z); else tmem_st16(tOw, z);
-  };
-  TileSeq seq(p);
-  int64_t tile = seq.next(p, bar);
-  if (tile >= 0) {
-    put_q(decode_tile(p, tile));
-    zero_o();
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(bar.q_full);
-      mbar_arrive(bar.o_empty);
-    }
-  }
-  for (int64_t next_tile; tile >= 0; tile = next_tile, ++it) {
-    const Tile t = decode_tile(p, tile);
-    const int owner = static_cast<int>(chunk & 1);
-    float m_use[2], l_run[2] = {0.f, 0.f};
-    bool over = false;
-    uint32_t sv[32];
-    if (g != owner) {
-      asm volatile("bar.sync 2, 512;" ::: "memory");
-      m_use[0] = xm[r0];
-      m_use[1] = xm[r0 + 8];
-    }
-    for (int j = (g - owner) & 1; j < t.nchunks; j += 2) {
-      const uint32_t c = chunk + j;
-      const uint32_t tS = tmem + TM_S + g * 128 + lanes16;
-      mbar_wait(&bar.s_full[g], (c >> 1) & 1);
-      tc_fence_after();
-      const int nvalid = min(BN, t.count - j * BN);
-      if (j == 0) {  // the tile's fixed row max: exact max of its first chunk
-        float mr[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          tmem_ld16x256_x8(tS + 64 * hh, sv);
-          tmem_ld_wait();
-          if (nvalid < BN) mask_half(sv, 64 * hh, nvalid, a);
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              mr[r] = fmax3f(mr[r], __uint_as_float(sv[4 * k + 2 * r]), __uint_as_float(sv[4 * k + 2 * r + 1]));
-        }
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          float m = mr[r];
-          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-          m_use[r] = m * sl2;
-          if (a == 0) xm[r0 + 8 * r] = m_use[r];
-        }
-        asm volatile("bar.arrive 2, 512;" ::: "memory");
-      }
-      float2 sum2[2][2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) sum2[r][0] = sum2[r][1] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        tmem_ld16x256_x8(tS + 64 * hh, sv);
-        tmem_ld_wait();
-        if (nvalid < BN) mask_half(sv, 64 * hh, nvalid, a);
-        uint32_t pk[16];
-        exp_half<D>(sv, sl2, m_use, pk, sum2);
-        tmem_st16x128_x8(tS + 32 * hh, pk);
-      }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const float2 s = __fadd2_rn(sum2[r][0], sum2[r][1]);
-        const float sr = s.x + s.y;
-        over |= !(sr <= 1.8446744e19f);  // 2^64
-        l_run[r] += sr;
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar.p_full[g]);
-    }
-    if (over && p.status != nullptr) atomicOr(p.status, 16);
-    chunk += t.nchunks;
-    // ---- epilogue.  l partials: quad sum, one slot per group; the barrier also tells every
-    //      warp that both groups have consumed every S of the tile, so Q may be replaced.
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 1);
-      l_run[r] += __shfl_xor_sync(0xffffffffu, l_run[r], 2);
-      if (a == 0) {
-        xch[128 + 128 * g + r0 + 8 * r] = l_run[r];
-        if (g == 0) xch[384 + r0 + 8 * r] = m_use[r];
-      }
-    }
-    softmax_bar();
-    const int row = q * 32 + lane;
-    const float lrow = xch[128 + row] + xch[256 + row], mrow = xch[384 + row];
-    next_tile = seq.next(p, bar);
-    if (next_tile >= 0) {
-      put_q(decode_tile(p, next_tile));
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar.q_full);
-    }
-    const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
-    mbar_wait(bar.o_full, it & 1);
-    tc_fence_after();
-    const bool valid = row < t.rows;
-    const int64_t out_row = static_cast<int64_t>(t.row0) + t.q0 + row;
-    uint32_t o[NOC];
-    if constexpr (NOC == 32) tmem_ld32(tOw, o); else tmem_ld16(tOw, o);
-    tmem_ld_wait();
-    zero_o();
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar.o_empty);
-    if (valid) store_row<OUT_F32, NOC>(p.out, out_row * D + part * NOC, o, inv);
-    if (part == 0 && valid && p.lse != nullptr)
-      p.lse[out_row] = lrow > 0.f ? mrow * 0.69314718055994531f + logf(lrow) : -INFINITY;
-    softmax_bar();  // xch read by every warp before the next tile writes it
-  }
-}
-#endif
-
 template <int D, bool OUT_F32>
 __global__ void __launch_bounds__(32 * NWARPS, 1)
     fga_attn_ws_kernel(const __grid_constant__ CUtensorMap tmK2, const __grid_constant__ CUtensorMap tmV2,
@@ -842,7 +643,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar.s_full[i], 1);
-      mbar_init(&bar.p_full[i], PGRP);
+      mbar_init(&bar.p_full[i], NSOFT);
       mbar_init(&bar.pv_done[i], 1);
     }
     mbar_init(bar.q_full, NSOFT);
@@ -866,17 +667,6 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
   if (p.trace != nullptr && tid == 0 && blockIdx.x < 1024) p.trace[FGA_TRACE_CTA_OFF + 2 * blockIdx.x] = global_ns();
   record_cta_ns(p, 0);
 
-#if FGA_WS2
-  if (warp < NSOFT) {
-    softmax2<D, OUT_F32>(p, qptr, bar, tmem, tid, reinterpret_cast<float*>(smem + L::OFF_XCH));
-  } else if (warp < WARP_PROD0) {
-    mma_chain<D>(p, smem, bar, tmem, warp - WARP_MMA0);
-  } else if (warp < WARP_PROD0 + NPROD) {
-    producer_half<D>(p, &tmK2, &tmV2, smem, bar, (warp - WARP_PROD0) >> 1, (warp - WARP_PROD0) & 1, lane);
-  } else if (warp == WARP_SCHED && p.sched != nullptr && lane == 0) {
-    tile_scheduler(p, bar);
-  }
-#else
   static_assert(NWARPS % 4 == 0, "whole warpgroups are needed for setmaxnreg");
   // setmaxnreg.inc can only take registers this CTA released with .dec (its pool is threads x launch regs)
   constexpr int kThreads = 32 * NWARPS;
@@ -896,7 +686,6 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
       tile_scheduler(p, bar);
     }
   }
-#endif
   tc_fence_before();
   __syncthreads();
   if (p.trace != nullptr && tid == 0 && blockIdx.x < 1024) p.trace[FGA_TRACE_CTA_OFF + 2 * blockIdx.x + 1] = global_ns();
