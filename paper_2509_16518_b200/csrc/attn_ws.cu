@@ -28,7 +28,8 @@
 //         128B-swizzled ring slots (3 K + 3 V)
 //   14    tile scheduler: claims tiles from a global counter (atomicAdd, in the order of
 //         p.order when given: the host's per-head longest-first order) and hands them to every
-//         role through a 16-entry shared ring, so CTAs that draw short lists take more tiles
+//         role through a 2-entry shared ring (one tile claimed ahead), so CTAs that draw short
+//         lists take more tiles
 //   15    idle
 // TMEM (512 cols): O [0, D) | Q [128, 128 + D/2) | S0 [256, 384) | S1 [384, 512).
 // P_j (bf16 pairs) overwrites S[j%2] cols 0..63.
@@ -55,7 +56,10 @@ constexpr int WARP_MMA0 = 8;  // MMA issuers 8 (buffer 0) and 9 (buffer 1)
 constexpr int WARP_PROD0 = 10;
 constexpr int NPROD = 4;      // gather producers 10-13
 constexpr int WARP_SCHED = 14;
-constexpr int NSCHED = 16;    // tile ring entries
+#ifndef FGA_NSCHED
+#define FGA_NSCHED 2  // 16 (round-2 first cut) claimed 16 tiles per CTA up front: tail 1.10 vs 1.02
+#endif
+constexpr int NSCHED = FGA_NSCHED;  // tile ring entries = how far the scheduler claims ahead
 constexpr int NCONSUMERS = NSOFT + 2 + NPROD;  // warps that read every tile ring entry
 constexpr int NWARPS = 16;
 constexpr int REG_SOFTMAX = 184;
