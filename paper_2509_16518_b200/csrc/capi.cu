@@ -339,13 +339,17 @@ int fga_build_mask_avgq(const void* q, const void* k, fga_shape shape, int strat
     const int64_t words = (n + 31) / 32;
     PooledOut out;
     out.keep_bits = pw.take<uint32_t>(rows * words);
-    out.amax = pw.take<unsigned long long>(rows);
+    out.fix_rows = pw.take<int32_t>(rows);
+    out.fix_count = pw.take<int32_t>(1);
     out.tau = tau;
-    if (out.keep_bits == nullptr || out.amax == nullptr)
+    out.idx = idx;
+    out.idx_stride = idx_stride;
+    out.counts = counts;
+    out.fill = fill_sentinel;
+    if (out.keep_bits == nullptr || out.fix_rows == nullptr || out.fix_count == nullptr)
       return fail(FGA_EINVAL, "build_mask_avgq: workspace too small (fga_workspace_bytes)");
-    if (cudaMemsetAsync(out.amax, 0, sizeof(unsigned long long) * rows, st) != cudaSuccess) return check_launch("memset");
-    if ((rc = launch_pooled_scores(q, k, shape, 1, out, w, st)) != FGA_OK) return rc;
-    return launch_compact_bits(out.keep_bits, rows, n, idx, idx_stride, counts, fill_sentinel, st, out.amax);
+    if (cudaMemsetAsync(out.fix_count, 0, sizeof(int32_t), st) != cudaSuccess) return check_launch("memset");
+    return launch_pooled_scores(q, k, shape, 1, out, w, st);  // scores -> keep bits -> lists -> argmax fix-up
   }
   if (round_bf16 && n <= FGA_SELECT_MAX_N) {  // bf16 scores -> fused selection + compaction
     Workspace pw = w;

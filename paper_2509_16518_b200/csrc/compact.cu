@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(256) fga_pack_bits_kernel(const uint8_t* __res
 __global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_bits_kernel(const uint32_t* __restrict__ bits, int64_t words,
                                                                      int64_t n, int32_t* __restrict__ idx,
                                                                      int64_t stride, int32_t* __restrict__ counts,
-                                                                     int fill, const unsigned long long* __restrict__ amax) {
+                                                                     int fill, int32_t* __restrict__ fix_rows,
+                                                                     int32_t* __restrict__ fix_count) {
   __shared__ int s_warp[2][WARPS];
   __shared__ uint16_t s_stage[WARPS * BUFS][STEP];
   const int64_t row = blockIdx.x;
@@ -265,8 +266,8 @@ __global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_bits_kern
   int32_t* out = idx + row * stride;
   const BitSrc src{bits + row * words, words, n, tid & 31};
   int running = compact_row(src, (words + 31) / 32, out, s_warp, s_stage);
-  if (running == 0 && amax != nullptr) {  // argmax fallback of a fused threshold pass (masks.py:86-87)
-    if (tid == 0) out[0] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(amax[row] & 0xFFFFFFFFull));
+  if (running == 0 && fix_rows != nullptr) {  // argmax fallback of a fused threshold pass (masks.py:86-87):
+    if (tid == 0) fix_rows[atomicAdd(fix_count, 1)] = static_cast<int32_t>(row);  // out[0] by the fix-up
     running = 1;
   }
   if (tid == 0) counts[row] = running;
@@ -287,13 +288,13 @@ int launch_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bit
 }
 
 int launch_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx, int64_t idx_stride,
-                        int32_t* counts, int fill, cudaStream_t stream, const unsigned long long* amax) {
+                        int32_t* counts, int fill, cudaStream_t stream, int32_t* fix_rows, int32_t* fix_count) {
   if (rows < 0 || n <= 0 || idx_stride < n) return fail(FGA_EINVAL, "compact_bits: need rows >= 0, n > 0, idx_stride >= n");
   if (n >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact_bits: n must be < 2^31");
   if (rows == 0) return FGA_OK;
   if (rows >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact_bits: too many rows");
   fga_compact_bits_kernel<<<static_cast<unsigned>(rows), WARPS * 32, 0, stream>>>(bits, (n + 31) / 32, n, idx, idx_stride,
-                                                                           counts, fill, amax);
+                                                                           counts, fill, fix_rows, fix_count);
   return check_launch("fga_compact_bits_kernel");
 }
 

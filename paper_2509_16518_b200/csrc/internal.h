@@ -76,25 +76,44 @@ int launch_gather_probe(const void* k, const void* v, int64_t n, int64_t d, cons
 int launch_gather(const void* matrix, int64_t rows, int64_t d, const int32_t* indices, int64_t n_idx, void* out,
                   cudaStream_t stream);
 int launch_pack_bits(const uint8_t* keep, int64_t rows, int64_t n, uint32_t* bits, cudaStream_t stream);
+// fix_rows / fix_count (nullable): rows with no bit set are listed there (count 1, idx[0] left to the
+// caller's argmax pass) instead of getting count 0.
 int launch_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* idx, int64_t idx_stride,
-                        int32_t* counts, int fill, cudaStream_t stream, const unsigned long long* amax = nullptr);
+                        int32_t* counts, int fill, cudaStream_t stream, int32_t* fix_rows = nullptr,
+                        int32_t* fix_count = nullptr);
 int launch_fgm1_unpack(const int32_t* words, const int64_t* starts, int64_t rows, int64_t n, int32_t* idx,
                        int64_t idx_stride, int32_t* counts, int fill, cudaStream_t stream);
 int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s, int round, float* gmax,
                                float* row_max, float* row_rinv, cudaStream_t st);
 // Outputs of the avg-query pooled-score pass (exactly one of scores / scores16 / keep_bits):
 // fp32 scores, bf16 scores, or the threshold decision fused into the epilogue -- keep bits
-// (bit b of word w of row r = key 32w + b) plus amax[r] = max over the row of
-// (order-preserving bf16 key << 32 | ~key index), the argmax fallback (callers zero amax first).
+// (bit b of word w of row r = key 32w + b), compacted into idx / counts, rows that keep nothing
+// listed in fix_rows (fix_count zeroed by the caller) and given their argmax key by a fix-up pass.
 struct PooledOut {
   float* scores = nullptr;
   uint16_t* scores16 = nullptr;
   uint32_t* keep_bits = nullptr;
-  unsigned long long* amax = nullptr;
   float tau = 0.f;
+  int32_t* idx = nullptr;  // keep_bits: the compacted lists
+  int64_t idx_stride = 0;
+  int32_t* counts = nullptr;
+  int fill = 0;
+  int32_t* fix_rows = nullptr;   // [rows]
+  int32_t* fix_count = nullptr;  // [1]
 };
-int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, const void* k, const fga_shape& s, int round,
-                            const PooledOut& out, cudaStream_t st);
+// parts_ready: the three bf16 parts of q̄ are already in parts (pooled_mean_bulk_kernel), else split here
+int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, bool parts_ready, const void* k,
+                            const fga_shape& s, int round, const PooledOut& out, cudaStream_t st);
+// q̄ value v -> parts[i], parts[n + i], parts[2n + i] (bf16, hi + mid + lo == v exactly)
+__device__ __forceinline__ void split3(float v, __nv_bfloat16* parts, int64_t n, int64_t i) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(hi);
+  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+  parts[i] = hi;
+  parts[n + i] = mid;
+  parts[2 * n + i] = lo;
+}
 int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int round, const PooledOut& out,
                          Workspace& ws, cudaStream_t st);
 int launch_cached_group_max(const void* q, const void* k, const fga_shape& s, int round, float* gmax, Workspace& ws,

@@ -42,10 +42,12 @@ __global__ void pooled_mean_kernel(const __nv_bfloat16* __restrict__ q, float* _
 
 // Same sums (each column added row by row, in order) with the group's rows -- one contiguous
 // M x D bf16 block -- brought into shared memory by TMA bulk copies first: one CTA of D threads
-// per group, thread = column.  Used when the block is 16-byte aligned and fits in 64 KB.
+// per group, thread = column.  Used when the block is 16-byte aligned and fits in 64 KB.  With
+// parts != null it also writes the three bf16 parts of q̄ the tensor-core score pass reads
+// (split3_kernel's split, parts_n = B*H*G*D elements per part).
 constexpr int PM_MAX_BYTES = 64 * 1024;
 __global__ void pooled_mean_bulk_kernel(const __nv_bfloat16* __restrict__ q, float* __restrict__ qbar, int N, int D,
-                                        int M, int G) {
+                                        int M, int G, __nv_bfloat16* __restrict__ parts, int64_t parts_n) {
   extern __shared__ __align__(16) __nv_bfloat16 s_rows[];
   __shared__ __align__(8) uint64_t bar;
   const int64_t bhg = blockIdx.x;
@@ -69,7 +71,9 @@ __global__ void pooled_mean_bulk_kernel(const __nv_bfloat16* __restrict__ q, flo
   float acc = 0.f;
 #pragma unroll 8
   for (int i = 0; i < hi - lo; ++i) acc = __fadd_rn(acc, __bfloat162float(s_rows[i * D + d]));
-  qbar[bhg * D + d] = __fdiv_rn(acc, static_cast<float>(hi - lo));
+  const float v = __fdiv_rn(acc, static_cast<float>(hi - lo));
+  qbar[bhg * D + d] = v;
+  if (parts != nullptr) split3(v, parts, parts_n, bhg * D + d);
 }
 
 // 64x64 fp32 tile of A[rows, D] . B[cols, D]^T, 256 threads, 4x4 per thread.
@@ -529,6 +533,7 @@ int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int r
   __nv_bfloat16* parts = ws.take<__nv_bfloat16>(3 * B * H * G * D);
   if (qbar == nullptr || parts == nullptr) return fail(FGA_EINVAL, "pooled_scores: workspace too small (fga_workspace_bytes)");
   const int64_t blk = M * D * 2;
+  bool parts_ready = false;
   if (D % 8 == 0 && D <= 1024 && blk <= PM_MAX_BYTES && (reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
     if (const int rc = smem_opt_in(reinterpret_cast<const void*>(pooled_mean_bulk_kernel), static_cast<int>(blk),
                                    "pooled_mean_bulk");
@@ -536,7 +541,8 @@ int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int r
       return rc;
     pooled_mean_bulk_kernel<<<static_cast<unsigned>(B * H * G), static_cast<unsigned>(D), static_cast<size_t>(blk),
                               st>>>(static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N),
-                                    static_cast<int>(D), static_cast<int>(M), static_cast<int>(G));
+                                    static_cast<int>(D), static_cast<int>(M), static_cast<int>(G), parts, B * H * G * D);
+    parts_ready = true;
   } else {
     pooled_mean_kernel<<<static_cast<unsigned>(B * H * G), 128, 0, st>>>(
         static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N), static_cast<int>(D), static_cast<int>(M),
@@ -544,7 +550,7 @@ int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int r
   }
   const char* cc = std::getenv("FGA_POOLED_CC");  // 1: the CUDA-core tile kernel below
   if (out.keep_bits != nullptr || cc == nullptr || cc[0] != '1') {
-    const int rc = launch_pooled_scores_tc(qbar, parts, k, s, round, out, st);
+    const int rc = launch_pooled_scores_tc(qbar, parts, parts_ready, k, s, round, out, st);
     if (rc != FGA_EUNSUPPORTED || out.keep_bits != nullptr) return rc;  // fused bits: tensor-core pass only
   }
   const float scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));

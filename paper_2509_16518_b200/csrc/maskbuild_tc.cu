@@ -30,6 +30,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "attn_common.cuh"
 #include "internal.h"
@@ -52,9 +54,10 @@ constexpr int CB_P1G = 2;  // pass 1: two groups per unit share every K chunk (h
 #endif
 // Q-side tiles per unit: pass 2 q̄ hi/mid/lo (accumulated into one score tile), pass 1 the unit's
 // CB_P1G groups (one score tile each), pass 0 one query tile
-constexpr int cb_nq(int pass) { return pass == 2 ? 3 : pass == 1 ? CB_P1G : 1; }
+// (pass 3 = the argmax fix-up of a fused threshold pass: pass 2's tiles for the rows listed)
+constexpr int cb_nq(int pass) { return pass >= 2 ? 3 : pass == 1 ? CB_P1G : 1; }
 constexpr int cb_sbw(int pass) { return pass == 1 ? 128 * CB_P1G : 128; }  // TMEM columns per S buffer
-constexpr int cb_ns(int pass) { return pass == 2 ? 3 : 4; }  // K ring slots
+constexpr int cb_ns(int pass) { return pass >= 2 ? 3 : 4; }  // K ring slots
 constexpr int CB_NS = 4;                                      // barrier slots (max ring)
 constexpr int CB_SB = 4;  // S buffers in TMEM (4 x 128 columns): the MMA runs up to 3 tiles ahead
 constexpr int CB_BARS = 2 + 2 * CB_NS + 2 * CB_SB;
@@ -105,10 +108,13 @@ struct CbParams {
   float* scores;      // pass 2: [B*H*G*N] fp32, or
   uint16_t* scores16; // pass 2: [B*H*G*N] bf16 bits (the builders' input; p.round must be 1), or
   uint32_t* keep_bits;            // pass 2: [B*H*G, words] threshold decisions (bf16 score >= tau)
-  unsigned long long* amax;       // pass 2 with keep_bits: [B*H*G] argmax key per row (atomicMax)
   float tau;
+  float a_mid, hb;                // pass 2 with keep_bits: accumulator threshold and band (threshold_band)
+  const int32_t* fix_rows;        // pass 3: rows (b*h*G + g) whose threshold kept nothing
+  const int32_t* fix_count;       //         their number (device)
+  int32_t* fix_idx;               //         idx[row * fix_stride] = the row's argmax key
+  int64_t fix_stride;
   int words;                      // ceil(N / 32)
-  int kslabs;         // pass 2: key ranges per (b*h, group tile)
   float scale;
   int round;
   float* row_max;  // [B*H*N]
@@ -126,20 +132,56 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
   extern __shared__ __align__(1024) uint8_t smem_cb[];
   uint8_t* smem = smem_cb;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
+  if (PASS == 3 && blockIdx.x >= *p.fix_count) return;  // (usually every CTA: no row kept nothing)
   const CbBars bar = cb_bars<D, PASS>(smem);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ks_n = PASS == 2 ? p.kslabs : 1;  // pass 2 also splits the keys over units (parallelism)
-  const int64_t n_units = p.bh * p.tiles * ks_n;
-  // unit u -> (b*h, tile t, key chunks [c_lo, c_hi))
+  const int64_t n_units = PASS == 3 ? static_cast<int64_t>(*p.fix_count) : p.bh * p.tiles;
+  // unit u of passes 0 and 3 -> (b*h, tile t, key chunks [c_lo, c_hi))
   auto unit = [&](int64_t u, int64_t& bh, int& t, int& c_lo, int& c_hi) {
-    const int ks = static_cast<int>(u % ks_n);
-    const int64_t r = u / ks_n;
-    bh = r / p.tiles;
-    t = static_cast<int>(r % p.tiles);
-    c_lo = static_cast<int>(static_cast<int64_t>(p.nch) * ks / ks_n);
-    c_hi = static_cast<int>(static_cast<int64_t>(p.nch) * (ks + 1) / ks_n);
+    if (PASS == 3) {  // one listed row: its group tile over every key chunk
+      const int r = __ldg(p.fix_rows + u);
+      bh = r / p.groups;
+      t = (r % p.groups) / BM;
+    } else {
+      bh = u / p.tiles;
+      t = static_cast<int>(u % p.tiles);
+    }
+    c_lo = 0;
+    c_hi = p.nch;
   };
-  const int nch = p.nch;  // key chunks per unit
+  // This CTA's units.  Passes 1 and 2 split the flattened (b*h, tile, key chunk) space into gridDim.x
+  // contiguous ranges (balanced to one chunk), cut at tile boundaries: a unit is a (b*h, tile)
+  // with a key chunk range.  Passes 0 (row statistics over every key) and 3 stride over whole units.
+  constexpr bool FLAT = PASS == 1 || PASS == 2;
+  const int64_t flat_n = p.bh * p.tiles * static_cast<int64_t>(p.nch);
+  struct Seq {
+    int64_t u, f, hi;
+  };
+  auto seq_init = [&]() {
+    Seq q;
+    q.u = blockIdx.x;
+    q.f = flat_n * blockIdx.x / gridDim.x;
+    q.hi = flat_n * (blockIdx.x + 1) / gridDim.x;
+    return q;
+  };
+  auto seq_next = [&](Seq& q, int64_t& bh, int& t, int& c_lo, int& c_hi, int64_t& uid) -> bool {
+    uid = q.u;
+    if (FLAT) {
+      if (q.f >= q.hi) return false;
+      const int64_t r = q.f / p.nch;
+      bh = r / p.tiles;
+      t = static_cast<int>(r % p.tiles);
+      c_lo = static_cast<int>(q.f % p.nch);
+      c_hi = static_cast<int>(min(static_cast<int64_t>(p.nch), c_lo + (q.hi - q.f)));
+      q.f += c_hi - c_lo;
+      ++q.u;
+      return true;
+    }
+    if (q.u >= n_units) return false;
+    unit(q.u, bh, t, c_lo, c_hi);
+    q.u += gridDim.x;
+    return true;
+  };
   if (tid == 0) {
     prefetch_tmap(&tmQ);
     prefetch_tmap(&tmK);
@@ -170,16 +212,16 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       const uint64_t pol_q = policy_evict_first(), pol_k = policy_evict_last();
       uint32_t kc = 0;
       int it = 0;
-      for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-        int64_t bh;
-        int t, c_lo, c_hi;
-        unit(u, bh, t, c_lo, c_hi);
+      Seq sq = seq_init();
+      int64_t bh, u;
+      int t, c_lo, c_hi;
+      for (; seq_next(sq, bh, t, c_lo, c_hi, u); ++it) {
         const int row0 = static_cast<int>(bh * p.n);
         mbar_wait(bar.q_empty, (it & 1) ^ 1);
         mbar_expect_tx(bar.q_full, L::NQ * BM * D * 2);
 #pragma unroll
         for (int qp = 0; qp < L::NQ; ++qp) {
-          const int qrow = PASS == 2 ? static_cast<int>(qp * p.part_rows + bh * p.groups) + t * BM
+          const int qrow = PASS >= 2 ? static_cast<int>(qp * p.part_rows + bh * p.groups) + t * BM
                                      : row0 + (t * L::NQ + qp) * BM;  // pass 1: group CB_P1G*t + qp
 #pragma unroll
           for (int h = 0; h < D / 64; ++h)
@@ -203,10 +245,10 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
     const uint64_t dk0 = sdesc_sw128(smem_u32(smem + L::OFF_K), 16, 1024);
     uint32_t kc = 0, sc = 0;
     int it = 0;
-    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-      int64_t bh;
-      int t, c_lo, c_hi;
-      unit(u, bh, t, c_lo, c_hi);
+    Seq sq = seq_init();
+    int64_t bh, u;
+    int t, c_lo, c_hi;
+    for (; seq_next(sq, bh, t, c_lo, c_hi, u); ++it) {
       mbar_wait(bar.q_full, it & 1);
       for (int c = c_lo; c < c_hi; ++c, ++kc, ++sc) {
         const uint32_t slot = kc % L::NS, use = kc / L::NS, b = sc % L::NSB;
@@ -248,13 +290,20 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
     float* const s32 = p.scores;
     uint32_t* const bits_out = p.keep_bits;
     const uint32_t tau_b16 = __bfloat16_as_ushort(__float2bfloat16_ru(p.tau));  // p.tau > 0
+    const float a_mid = p.a_mid, hb = p.hb;
     const float sl0 = scale * 1.4426950408889634f;  // pass 0: scale * log2e
-    (void)rnd; (void)s16; (void)s32; (void)bits_out; (void)tau_b16;
+    (void)rnd; (void)s16; (void)s32; (void)bits_out; (void)tau_b16; (void)a_mid; (void)hb;
+    // s = fl(fl(expf(fl(acc * scale))) / D), bf16 bits (masks.py:108-118, rounded as core.py:196-200)
+    auto score_b16 = [&](float acc) {
+      constexpr float inv_d = 1.0f / D;  // D is a power of two: x / D == x * (1/D) exactly
+      return static_cast<uint32_t>(
+          __bfloat16_as_ushort(__float2bfloat16_rn(__fmul_rn(expf(__fmul_rn(acc, scale)), inv_d))));
+    };
     uint32_t sc = 0;
-    for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-      int64_t bh;
-      int t, c_lo, c_hi;
-      unit(u, bh, t, c_lo, c_hi);
+    Seq sq = seq_init();
+    int64_t bh, u;
+    int t, c_lo, c_hi;
+    for (; seq_next(sq, bh, t, c_lo, c_hi, u);) {
       const int64_t row0 = bh * p.n;
       const int q0 = t * L::NQ * BM;  // pass 1: the first query of the unit's first group
       if (PASS == 1) {
@@ -279,10 +328,32 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       float m = -INFINITY;
       float ml0 = -INFINITY;  // pass 0: m * log2e
       double den = 0.0;
+      // pass 3: the listed row's group column and this thread's best (bf16 score + 1, key) so far
+      const int fix_r = PASS == 3 ? __ldg(p.fix_rows + u) : 0;
+      const int fix_col = (fix_r % (p.groups > 0 ? p.groups : 1)) % BM;
+      uint32_t best_rank = 0, best_j = 0xFFFFFFFFu;
       for (int c = c_lo; c < c_hi; ++c, ++sc) {
         const uint32_t b = sc % L::NSB;
         mbar_wait(&bar.s_full[b], (sc / L::NSB) & 1);
         tc_fence_after();
+        if constexpr (PASS == 3) {
+          // exact score of key j for the row's group (the fused pass's arithmetic), running argmax:
+          // highest bf16 bits (NaN above inf, as np.argmax), the smallest key among equals
+          if (w == fix_col / 32) {
+            const uint32_t x = tmem_ld1(tmem + (static_cast<uint32_t>(q * 32) << 16) + b * L::SBW + fix_col);
+            tmem_ld_wait();
+            const int j = c * BN + row;
+            const uint32_t rank = score_b16(__uint_as_float(x)) + 1u;
+            if (j < n_keys && rank > best_rank) {
+              best_rank = rank;
+              best_j = static_cast<uint32_t>(j);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar.s_empty[b]);
+          continue;
+        }
         uint32_t v[32];
         tmem_ld32(tl + b * L::SBW, v);
         tmem_ld_wait();
@@ -306,29 +377,32 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             // s = fl(fl(expf(fl(acc * scale))) / D); one pointer step of n per group column, no
             // per-element predicate for a full 32-group slice
             if (bits_out != nullptr) {
-              // threshold fused into the epilogue (masks.py:131-132): per group column one ballot of
-              // this warp's 32 consecutive keys -> keep word; the bf16 score's order-preserving key
-              // and the key index reduced for the argmax fallback (masks.py:86-87)
-              const int g0 = t * BM + w * 32;
-              uint32_t myword = 0, mybest = 0;
+              // threshold fused into the epilogue (masks.py:131-132), per group column one ballot of
+              // this warp's 32 consecutive keys -> keep word.  The bf16 score is a non-decreasing
+              // function of the accumulator, and outside a narrow band around a_mid (threshold_band)
+              // "score >= tau" is exactly "acc >= a_mid": one compare per score.  A 32 x 32 block
+              // with an accumulator in the band (or a NaN) is evaluated exactly.  Rows that keep
+              // nothing get their argmax from the pass-3 fix-up (masks.py:86-87).
+              bool band = false;
 #pragma unroll
-              // scores are exp(.)/D >= 0 (or NaN), so their bf16 bits order like their values and
-              // s >= tau <=> bits >= bits(tau rounded up to bf16)
-              for (int k = 0; k < 32; ++k) {
-                const uint32_t b16 = __bfloat16_as_ushort(
-                    __float2bfloat16_rn(__fmul_rn(expf(__fmul_rn(__uint_as_float(v[k]), scale)), inv_d)));
-                const uint32_t word = __ballot_sync(0xffffffffu, b16 >= tau_b16 && b16 <= 0x7F80u);
-                const uint32_t best = __reduce_max_sync(0xffffffffu, (b16 << 16) | (31u - lane));
-                if (lane == k) { myword = word; mybest = best; }
+              for (int k = 0; k < 32; ++k) band |= !(fabsf(__uint_as_float(v[k]) - a_mid) >= hb);
+              uint32_t* xw = reinterpret_cast<uint32_t*>(smem + L::OFF_XCH) + warp * 32;
+              if (__any_sync(0xffffffffu, band)) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                  const uint32_t b16 = score_b16(__uint_as_float(v[k]));
+                  xw[k] = __ballot_sync(0xffffffffu, b16 >= tau_b16 && b16 <= 0x7F80u);
+                }
+              } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) xw[k] = __ballot_sync(0xffffffffu, __uint_as_float(v[k]) >= a_mid);
               }
-              const int g = g0 + lane;
-              if (g < p.groups && c * BN + q * 32 < n_keys) {  // a word past N belongs to no row
-                const int64_t row_g = bh * p.groups + g;
-                bits_out[row_g * p.words + (c * BN + q * 32) / 32] = myword;
-                const uint32_t jb = static_cast<uint32_t>(c * BN + q * 32) + (31u - (mybest & 31u));
-                atomicMax(p.amax + row_g, (static_cast<unsigned long long>((mybest >> 16) | 0x8000u) << 32) |
-                                              (0xFFFFFFFFu - jb));
-              }
+              __syncwarp();
+              const uint32_t myword = xw[lane];
+              __syncwarp();
+              const int g = t * BM + w * 32 + lane;
+              if (g < p.groups && c * BN + q * 32 < n_keys)  // a word past N belongs to no row
+                bits_out[(bh * p.groups + g) * p.words + (c * BN + q * 32) / 32] = myword;
             } else if (s16 != nullptr) {
               uint16_t* dst = s16 + off;
               if (kmax == 32) {
@@ -516,6 +590,27 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
           }
         }
       }
+      if (PASS == 3) {
+        uint32_t* xu = reinterpret_cast<uint32_t*>(smem + L::OFF_XCH);
+        if (w == fix_col / 32) {
+          const uint32_t mr = __reduce_max_sync(0xffffffffu, best_rank);
+          const uint32_t mj = __reduce_min_sync(0xffffffffu, best_rank == mr ? best_j : 0xFFFFFFFFu);
+          if (lane == 0) {
+            xu[2 * q] = mr;
+            xu[2 * q + 1] = mj;
+          }
+        }
+        epi_bar();
+        if (tid == 0) {
+          uint32_t mr = xu[0], mj = xu[1];
+          for (int o = 1; o < 4; ++o)
+            if (xu[2 * o] > mr || (xu[2 * o] == mr && xu[2 * o + 1] < mj)) {
+              mr = xu[2 * o];
+              mj = xu[2 * o + 1];
+            }
+          p.fix_idx[fix_r * p.fix_stride] = static_cast<int32_t>(mj);
+        }
+      }
       epi_bar();  // exchange / table space free for the next unit
     }
   }
@@ -534,7 +629,10 @@ int launch_pass(const CUtensorMap* maps, const CbParams& p, cudaStream_t st) {
   if (const int rc = smem_opt_in(reinterpret_cast<const void*>(kern), smem, "cached_tc"); rc != FGA_OK)
     return rc;
   const int sms = sm_count();
-  const int64_t units = p.bh * p.tiles * (PASS == 2 ? p.kslabs : 1);
+  // pass 3: the listed rows are counted on the device; at most one CTA per row
+  // passes 1 and 2: one contiguous range of (b*h, tile, key chunk) per CTA; pass 3: listed rows
+  // (counted on the device), at most one CTA per row
+  const int64_t units = PASS == 3 ? p.bh * p.groups : PASS == 0 ? p.bh * p.tiles : p.bh * p.tiles * p.nch;
   kern<<<static_cast<unsigned>(units < sms ? units : sms), 32 * CB_WARPS, smem, st>>>(maps[0], maps[1], p);
   return check_launch("cached_tc_kernel");
 }
@@ -573,34 +671,60 @@ int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s,
   return rc;
 }
 
+// Accumulator threshold of the fused threshold epilogue (pass 2 with keep_bits).  keep <=>
+// bf16_rn(y) >= t with t = tau rounded up to bf16 and y = fl(E / D), E = expf(s), s = fl(acc * scale).
+// Round-to-nearest-even gives bf16_rn(y) >= t for y > mid and < t for y < mid, mid = (t_prev + t) / 2
+// (a float); y = E / D exactly while E / D is normal (D is a power of two); expf is within 2 ulp of
+// e^s.  So with L = ln(mid * D): s > L + d  =>  E > mid * D  =>  kept, and s < L - d  =>  not kept,
+// for any d well above 2 ulp.  a_mid = L / scale and hb = 2e-5 max(1, |L|) / scale leave d >= 1.9e-5
+// after the roundings of acc * scale, a_mid and acc - a_mid; accumulators within hb of a_mid (about
+// 1e-5 of them at unit-scale scores) are evaluated exactly.  Thresholds whose mid is subnormal or
+// near overflow put every accumulator in the band (hb = inf): exact everywhere.
+static void threshold_band(float tau, int d, float scale, float* a_mid, float* hb) {
+  uint32_t bits;
+  std::memcpy(&bits, &tau, 4);
+  uint32_t t16 = (bits >> 16) + ((bits & 0xFFFFu) != 0u ? 1u : 0u);  // round up (tau > 0)
+  auto bf = [](uint32_t h) {
+    const uint32_t b = h << 16;
+    float f;
+    std::memcpy(&f, &b, 4);
+    return static_cast<double>(f);
+  };
+  const double mid = t16 >= 0x7F80u ? 0.0 : 0.5 * (bf(t16) + bf(t16 - 1));
+  const char* ex = std::getenv("FGA_THRESHOLD_EXACT");  // 1: every score evaluated (tests / A/B)
+  if (!(mid >= std::ldexp(1.0, -120)) || mid * d > std::ldexp(1.0, 120) || (ex != nullptr && ex[0] == '1')) {
+    *a_mid = 0.f;
+    *hb = INFINITY;
+    return;
+  }
+  const double L = std::log(mid * d);
+  *a_mid = static_cast<float>(L / scale);
+  *hb = static_cast<float>(2e-5 * std::max(1.0, std::fabs(L)) / scale);
+}
+
 // q̄ (fp32) -> three bf16 parts with hi + mid + lo == q̄ exactly (8 + 8 + 8 significand bits),
 // so K q̄^T is three exact-product bf16 MMAs accumulated in fp32.
 __global__ void split3_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ parts, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float v = x[i];
-    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-    const float r1 = v - __bfloat162float(hi);
-    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-    parts[i] = hi;
-    parts[n + i] = mid;
-    parts[2 * n + i] = lo;
-  }
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    split3(x[i], parts, n, i);
 }
 
 // Avg-query scores s[b,h,g,j] = exp(k_j . q̄_g * scale) / D on the tensor cores (pass 2);
 // FGA_EUNSUPPORTED unless D is 64 or 128.  qbar: fp32 [B*H*G, D] (pooled_mean_kernel).
-int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, const void* k, const fga_shape& s, int round,
-                            const PooledOut& out, cudaStream_t st) {
+int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, bool parts_ready, const void* k,
+                            const fga_shape& s, int round, const PooledOut& out, cudaStream_t st) {
   const int64_t B = s.batch, H = s.heads, N = s.seq_len, D = s.head_dim, M = s.group_size;
   if (D != 64 && D != 128) return FGA_EUNSUPPORTED;
   const int64_t G = (N + M - 1) / M;
   const int64_t rows = B * H * N, qrows = B * H * G;
   if (rows >= (int64_t(1) << 31) || 3 * qrows >= (int64_t(1) << 31)) return FGA_EUNSUPPORTED;
-  split3_kernel<<<static_cast<unsigned>(std::min<int64_t>((qrows * D + 255) / 256, 148 * 16)), 256, 0, st>>>(
-      qbar, parts, qrows * D);
-  int rc = check_launch("split3_kernel");
+  int rc = FGA_OK;
+  if (!parts_ready) {
+    split3_kernel<<<static_cast<unsigned>(std::min<int64_t>((qrows * D + 255) / 256, 148 * 16)), 256, 0, st>>>(
+        qbar, parts, qrows * D);
+    rc = check_launch("split3_kernel");
+  }
   CUtensorMap maps[2];
   if (rc == FGA_OK) rc = make_tmap_bf16_2d(&maps[0], parts, 3 * qrows, D, 64, BM);
   if (rc == FGA_OK) rc = make_tmap_bf16_2d(&maps[1], k, rows, D, 64, BN);
@@ -615,14 +739,25 @@ int launch_pooled_scores_tc(const float* qbar, __nv_bfloat16* parts, const void*
     p.scores = out.scores;
     p.scores16 = out.scores16;
     p.keep_bits = out.keep_bits;
-    p.amax = out.amax;
     p.tau = out.tau;
+    if (out.keep_bits != nullptr) threshold_band(out.tau, static_cast<int>(D), s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D)), &p.a_mid, &p.hb);
     p.words = static_cast<int>((N + 31) / 32);
-    // enough (b*h, group tile, key range) units for every SM, each at least 8 key chunks
-    p.kslabs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(p.nch / 8, (4 * 148 + p.bh * p.tiles - 1) / (p.bh * p.tiles))));
     p.scale = s.scale > 0.f ? s.scale : 1.0f / std::sqrt(static_cast<float>(D));
     p.round = round;
     rc = D == 64 ? launch_pass<64, 2>(maps, p, st) : launch_pass<128, 2>(maps, p, st);
+    if (rc == FGA_OK && out.keep_bits != nullptr && out.idx != nullptr) {
+      rc = launch_compact_bits(out.keep_bits, qrows, N, out.idx, out.idx_stride, out.counts, out.fill, st,
+                               out.fix_rows, out.fix_count);
+      if (rc == FGA_OK) {  // argmax of the rows that kept nothing: their tiles again, exact scores
+        CbParams p3 = p;
+        p3.keep_bits = nullptr;
+        p3.fix_rows = out.fix_rows;
+        p3.fix_count = out.fix_count;
+        p3.fix_idx = out.idx;
+        p3.fix_stride = out.idx_stride;
+        rc = D == 64 ? launch_pass<64, 3>(maps, p3, st) : launch_pass<128, 3>(maps, p3, st);
+      }
+    }
   }
   return rc;
 }

@@ -223,3 +223,34 @@ def test_avg_query_builders_at_wan_shape_vs_oracle():
                 flip = np.setxor1d(have, want)
                 if b.strategy.endswith("threshold"):
                     assert mism[r, flip].all(), (b.strategy, r)  # and only at those keys
+
+
+@pytest.mark.parametrize("mode", ["quantile", "bf16_value", "midpoint", "tiny", "huge"])
+def test_fused_threshold_band_edges(mode, monkeypatch):
+    # the fused threshold decides most scores by one accumulator compare (threshold_band in
+    # maskbuild_tc.cu) and evaluates only a narrow band exactly: taus on a bf16 score value, on the
+    # rounding midpoint between two bf16 values, and degenerate ones (tiny / huge: everything
+    # exact) against the reference selection on the same scores, and against the all-exact
+    # evaluation (FGA_THRESHOLD_EXACT=1) bit for bit
+    n, d = 3000, 128
+    cfg = fga.AttnConfig(1, 2, n, d, precision="bf16")
+    g = torch.Generator(device="cuda").manual_seed(404)
+    q, k = (torch.randn(cfg.dims, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2))
+    rows = fga.pooled_query_scores(q, k, cfg).cpu().numpy().reshape(-1, n)
+    med = float(np.median(rows))
+    b16 = np.array([med], np.float32).view(np.uint32)[0] >> 16
+    val = float(np.array([b16 << 16], np.uint32).view(np.float32)[0])
+    prev = float(np.array([(b16 - 1) << 16], np.uint32).view(np.float32)[0])
+    tau = {"quantile": float(np.quantile(rows, 0.7)), "bf16_value": val, "midpoint": 0.5 * (val + prev),
+           "tiny": 1e-30, "huge": 1e30}[mode]
+    bc = fga.MaskBuilderConfig("avg_query_threshold", tau=tau)
+    m = fga.build_mask_avg_query(q, k, cfg, bc, device_result=True)
+    counts = m.counts.cpu().numpy().reshape(-1)
+    idx = m.idx.cpu().numpy().reshape(counts.size, -1)
+    for r in range(counts.size):
+        assert np.array_equal(idx[r, :counts[r]], _ref_threshold(rows[r], np.float32(tau))), (mode, r)
+    monkeypatch.setenv("FGA_THRESHOLD_EXACT", "1")
+    me = fga.build_mask_avg_query(q, k, cfg, bc, device_result=True)
+    assert torch.equal(me.counts, m.counts)
+    assert all(torch.equal(me.idx.view(counts.size, -1)[r, :c], m.idx.view(counts.size, -1)[r, :c])
+               for r, c in enumerate(counts.tolist()))
