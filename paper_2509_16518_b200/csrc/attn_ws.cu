@@ -162,11 +162,15 @@ struct TileSeq {
     }
     const uint32_t slot = i % NSCHED;
     mbar_wait(&bar.sched_full[slot], (i / NSCHED) & 1);
-    const int64_t t = *reinterpret_cast<volatile int64_t*>(&bar.sched_tile[slot]);
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&bar.sched_empty[slot]);
+    // lane 0 reads the entry and releases it (its read is ordered before its own arrival), the
+    // warp gets the id by shuffle
+    long long t = 0;
+    if ((threadIdx.x & 31) == 0) {
+      t = *reinterpret_cast<volatile int64_t*>(&bar.sched_tile[slot]);
+      mbar_arrive(&bar.sched_empty[slot]);
+    }
     ++i;
-    return t;
+    return __shfl_sync(0xffffffffu, t, 0);
   }
 };
 
