@@ -261,10 +261,17 @@ int64_t fga_workspace_bytes(int op, fga_shape shape, int round_bf16) {
       return static_cast<int64_t>(ws_pooled_bytes(shape));
     case FGA_WS_CACHED_GROUP_MAX:
       return static_cast<int64_t>(ws_cached_bytes(shape));
-    case FGA_WS_BUILD_AVGQ:
-      if (round_bf16 && shape.seq_len <= FGA_SELECT_MAX_N)
-        return static_cast<int64_t>(ws_pooled_bytes(shape) + Workspace::align(2 * cells));
-      return static_cast<int64_t>(ws_pooled_bytes(shape) + Workspace::align(4 * cells) + Workspace::align(cells));
+    case FGA_WS_BUILD_AVGQ: {
+      // fused threshold (keep bits + the list of rows that kept nothing + its count), or bf16
+      // scores for the selection kernel, or fp32 scores + keep bytes: the largest of the three
+      const int64_t rows = shape.batch * shape.heads * G;
+      const size_t fused = Workspace::align(4 * rows * ((shape.seq_len + 31) / 32)) + Workspace::align(4 * rows) +
+                           Workspace::align(4);
+      size_t rest = round_bf16 && shape.seq_len <= FGA_SELECT_MAX_N ? Workspace::align(2 * cells)
+                                                                     : Workspace::align(4 * cells) + Workspace::align(cells);
+      if (round_bf16 && fused > rest) rest = fused;
+      return static_cast<int64_t>(ws_pooled_bytes(shape) + rest);
+    }
     case FGA_WS_BUILD_CACHED:
       return static_cast<int64_t>(ws_cached_bytes(shape) + Workspace::align(4 * cells) + Workspace::align(cells));
     default:

@@ -70,6 +70,11 @@ def test_workspace_sizes_without_gpu():
     assert _lib.workspace_bytes(_lib.FGA_WS_BUILD_AVGQ, shp, 1) >= pooled + 2 * cells   # bf16 scores
     assert _lib.workspace_bytes(_lib.FGA_WS_BUILD_AVGQ, shp, 0) >= pooled + 5 * cells   # fp32 + keep bytes
     assert _lib.workspace_bytes(_lib.FGA_WS_BUILD_CACHED, shp) >= 5 * cells
+    # tiny rows: the fused threshold's keep bits + empty-row list + count (three 256-byte-aligned
+    # pieces) must fit even where the bf16 score buffer would be smaller
+    tiny = _lib.shape(1, 3, 1, 64, 1)
+    assert _lib.workspace_bytes(_lib.FGA_WS_BUILD_AVGQ, tiny, 1) >= \
+        _lib.workspace_bytes(_lib.FGA_WS_POOLED_SCORES, tiny) + 3 * 256
     assert _lib.load().fga_workspace_bytes(99, shp, 1) == _lib.FGA_EINVAL
     assert _lib.load().fga_workspace_bytes(1, _lib.shape(1, 1, 10, 64, 20), 1) == _lib.FGA_EINVAL
 
