@@ -352,12 +352,14 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
         if (r == 0) FGA_TS(p, it, j, 11);
         const uint32_t slot = c % NSV, use = c / NSV;
         mbar_wait(&bar.v_full[slot], use & 1);
+        if (r == 0) FGA_TS(p, it, j, 6);
         fence_proxy_async_smem();
         tc_fence_after();
         const uint64_t dv = dv0 + ((slot * L::KV) >> 4);
         // Deterministic accumulation: PV_c enters the tensor pipe only after PV_{c-1} (the other
         // issuer's) has been issued, so O sums the chunks in list order on every run.
         if (c > 0) mbar_wait(bar.pv_issued, (c - 1) & 1);
+        if (r == 0) FGA_TS(p, it, j, 7);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)

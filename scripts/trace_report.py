@@ -16,6 +16,10 @@ print("chunks traced", len(j), "MMA period per chunk (S issue)", (np.diff(t[r, 1
 print(" mma: waitK", (t[r, 9] - t[r, 8]).mean(), "fence", (t[r, 13] - t[r, 9]).mean(), "S issue+commit",
       (t[r, 14] - t[r, 13]).mean())
 print(" mma: waitP", (t[r, 11] - t[r, 10]).mean(), "PV(wait V+fence+issue+commit)", (t[r, 12] - t[r, 11]).mean())
+if (t[r, 6] > 0).all() and (t[r, 7] > 0).all():
+    print("   PV: wait V", (t[r, 6] - t[r, 11]).mean(), "wait PV_{c-1} issued", (t[r, 7] - t[r, 6]).mean(),
+          "issue+commit", (t[r, 12] - t[r, 7]).mean(), "| S: wait K", (t[r, 9] - t[r, 8]).mean(),
+          "issue+commit", (t[r, 14] - t[r, 9]).mean())
 sm = np.nonzero(t[:, 0] > 0)[0]
 s = sm[(sm >= 4) & (sm < sm.max() - 2)]
 print(" softmax(wg0) chunks", len(sm), "period per chunk", (np.diff(t[s, 5]) / np.diff(s)).mean() if len(s) > 1 else 0)

@@ -1,4 +1,5 @@
-"""Per-phase clock64 timeline of CTA 0's first tile (development aid)."""
+"""Per-phase clock64 timeline of CTA 0's tile FGA_TRACE_IT (development aid; needs a trace build,
+`_build.build_variant('trace', ['FGA_TRACE_ON=1'])`, run with FGA_LIB=build/variants/libtrace.so)."""
 import os
 import sys
 import time
@@ -9,6 +10,10 @@ T0 = time.time()
 def log(m):
     print(f"[{time.time() - T0:6.1f}s] {m}", flush=True)
 
+
+# the library reads FGA_TRACE once (first launch), so it is set before any call; every call is
+# traced and the last one's timeline is the file's content
+os.environ["FGA_TRACE"] = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/trace.txt"
 
 import torch
 
@@ -26,7 +31,6 @@ for _ in range(3):
     fga.sparse_attention(q, k, v, dm, cfg)
     torch.cuda.synchronize()
     log("warm-up call done")
-os.environ["FGA_TRACE"] = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/trace.txt"
 fga.sparse_attention(q, k, v, dm, cfg)
 torch.cuda.synchronize()
 log("traced call done")
