@@ -52,11 +52,15 @@ constexpr int CB_P1G = 1;  // pass 1: groups per unit (the exact-select variant 
 #else
 constexpr int CB_P1G = 2;  // pass 1: two groups per unit share every K chunk (half the L2 -> SMEM bytes)
 #endif
+#ifndef FGA_CB_P0G
+#define FGA_CB_P0G 1  // 2 measured slower: 3.6 -> 4.2 ms (bitwise the same output)
+#endif
+constexpr int CB_P0G = FGA_CB_P0G;  // pass 0: query tiles per unit sharing every K chunk
 // Q-side tiles per unit: pass 2 q̄ hi/mid/lo (accumulated into one score tile), pass 1 the unit's
-// CB_P1G groups (one score tile each), pass 0 one query tile
+// CB_P1G groups (one score tile each), pass 0 CB_P0G query tiles (one score tile each)
 // (pass 3 = the argmax fix-up of a fused threshold pass: pass 2's tiles for the rows listed)
-constexpr int cb_nq(int pass) { return pass >= 2 ? 3 : pass == 1 ? CB_P1G : 1; }
-constexpr int cb_sbw(int pass) { return pass == 1 ? 128 * CB_P1G : 128; }  // TMEM columns per S buffer
+constexpr int cb_nq(int pass) { return pass >= 2 ? 3 : pass == 1 ? CB_P1G : CB_P0G; }
+constexpr int cb_sbw(int pass) { return pass == 1 ? 128 * CB_P1G : pass == 0 ? 128 * CB_P0G : 128; }  // TMEM columns per S buffer
 constexpr int cb_ns(int pass) { return pass >= 2 ? 3 : 4; }  // K ring slots
 constexpr int CB_NS = 4;                                      // barrier slots (max ring)
 constexpr int CB_SB = 4;  // S buffers in TMEM (4 x 128 columns): the MMA runs up to 3 tiles ahead
@@ -74,7 +78,7 @@ struct CbSmem {
   static constexpr int OFF_NZ = OFF_TAB + CB_P1G * 128 * 16;  // pass 1: -(m_i + ln den_i) of the unit's groups
   static constexpr int OFF_XCH = OFF_NZ + CB_P1G * 128 * 4;     // pass 0: (m, den) per slice; pass 1: candidates x 2
   static constexpr int BYTES = OFF_XCH + 2 * 3 * CB_EW * 128 * 4;
-  static_assert(CB_EW * 128 * 12 <= 2 * 3 * CB_EW * 128 * 4, "exchange area");
+  static_assert(CB_P0G * CB_EW * 128 * 12 <= 2 * 3 * CB_EW * 128 * 4, "exchange area");
   static_assert(BYTES <= 232448, "exceeds the 227 KB of shared memory per CTA");
   static_assert(CB_BARS * 8 + 8 <= 256, "barrier area");
 };
@@ -263,7 +267,8 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             for (int kk = 0; kk < D / 16; ++kk) {
               const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
               const uint64_t dq = dq0 + ((qp * L::KV) >> 4) + off;
-              if (PASS == 0) umma_ss(tmem + b * L::SBW, dq, dk + off, IDESC, kk > 0 ? 1u : 0u);  // S = Q K^T
+              if (PASS == 0)  // S = Q K^T, one 128-column tile per query tile of the unit
+                umma_ss(tmem + b * L::SBW + qp * 128, dq, dk + off, IDESC, kk > 0 ? 1u : 0u);
               else if (PASS == 1)  // S^T = K Q_g^T, one 128-column tile per group of the unit
                 umma_ss(tmem + b * L::SBW + qp * 128, dk + off, dq, IDESC, kk > 0 ? 1u : 0u);
               else umma_ss(tmem + b * L::SBW, dk + off, dq, IDESC, (qp > 0 || kk > 0) ? 1u : 0u);
@@ -328,6 +333,8 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       float m = -INFINITY;
       float ml0 = -INFINITY;  // pass 0: m * log2e
       double den = 0.0;
+      float m_1 = -INFINITY, ml0_1 = -INFINITY;  // pass 0: the second query tile's row (CB_P0G == 2)
+      double den_1 = 0.0;
       // pass 3: the listed row's group column and this thread's best (bf16 score + 1, key) so far
       const int fix_r = PASS == 3 ? __ldg(p.fix_rows + u) : 0;
       const int fix_col = (fix_r % (p.groups > 0 ? p.groups : 1)) % BM;
@@ -357,7 +364,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
         uint32_t v[32];
         tmem_ld32(tl + b * L::SBW, v);
         tmem_ld_wait();
-        if (PASS != 1 || CB_P1G == 1) {  // (pass 1 reads its second group's tile first)
+        if ((PASS != 1 || CB_P1G == 1) && (PASS != 0 || CB_P0G == 1)) {  // (passes 0 / 1 read their second tile first)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar.s_empty[b]);
@@ -428,53 +435,64 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             }
           }
         } else if (PASS == 0) {
-          // columns: keys j = c*128 + 32w + k.  Each term exp(s - m) is one FFMA2 + MUFU ex2 on
-          // acc * scale * log2e - m * log2e; their rounding errors average out over the row's N
-          // terms, each chunk's 32 summed in fp32, the row in fp64.  m is a lazy running max (in
-          // the units of s = fl(acc * scale), attention_map's s): the exps use it until a score
-          // beats it by more than 8 log2 units, which shows up as a chunk sum above 2^8 (all terms
-          // are positive) and sends the warp to the exact path -- the chunk's max on the raw dot
-          // products (scale > 0 and rounding is monotonic, so fl(max(acc) * scale) = max(s)), den
-          // rescaled in fp64, the chunk re-summed.  Pass 1 needs only m + ln den, which any such m
-          // gives exactly; the per-chunk max and the fp64 exp are off the common path.
-          const int jbase = c * BN + w * 32;
-          if (jbase + 32 > n_keys) {
+          auto row_chunk = [&](uint32_t (&v)[32], float& m, float& ml0, double& den) {
+            // columns: keys j = c*128 + 32w + k.  Each term exp(s - m) is one FFMA2 + MUFU ex2 on
+            // acc * scale * log2e - m * log2e; their rounding errors average out over the row's N
+            // terms, each chunk's 32 summed in fp32, the row in fp64.  m is a lazy running max (in
+            // the units of s = fl(acc * scale), attention_map's s): the exps use it until a score
+            // beats it by more than 8 log2 units, which shows up as a chunk sum above 2^8 (all terms
+            // are positive) and sends the warp to the exact path -- the chunk's max on the raw dot
+            // products (scale > 0 and rounding is monotonic, so fl(max(acc) * scale) = max(s)), den
+            // rescaled in fp64, the chunk re-summed.  Pass 1 needs only m + ln den, which any such m
+            // gives exactly; the per-chunk max and the fp64 exp are off the common path.
+            const int jbase = c * BN + w * 32;
+            if (jbase + 32 > n_keys) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k)
-              if (jbase + k >= n_keys) v[k] = __float_as_uint(-INFINITY);
-          }
-          auto chunk_sum = [&](float ml) {
+              for (int k = 0; k < 32; ++k)
+                if (jbase + k >= n_keys) v[k] = __float_as_uint(-INFINITY);
+            }
+            auto chunk_sum = [&](float ml) {
+              float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+              for (int k = 0; k < 32; k += 2) {
+                const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
+                                            make_float2(sl0, sl0), make_float2(-ml, -ml));
+                if (CB_POLY > 0 && (k / 2) % (CB_POLY > 0 ? CB_POLY : 1) == CB_POLY - 1)
+                  acc = __fadd2_rn(acc, ex2_poly2<5>(x));  // this pair on the FMA pipe
+                else
+                  acc = __fadd2_rn(acc, make_float2(ex2(x.x), ex2(x.y)));
+              }
+              return acc;
+            };
             float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int k = 0; k < 32; k += 2) {
-              const float2 x = __ffma2_rn(make_float2(__uint_as_float(v[k]), __uint_as_float(v[k + 1])),
-                                          make_float2(sl0, sl0), make_float2(-ml, -ml));
-              if (CB_POLY > 0 && (k / 2) % (CB_POLY > 0 ? CB_POLY : 1) == CB_POLY - 1)
-                acc = __fadd2_rn(acc, ex2_poly2<5>(x));  // this pair on the FMA pipe
-              else
-                acc = __fadd2_rn(acc, make_float2(ex2(x.x), ex2(x.y)));
+            bool exact = m == -INFINITY;
+            if (!exact) {
+              acc = chunk_sum(ml0);
+              exact = !(acc.x + acc.y <= 256.f);
             }
-            return acc;
+            if (__any_sync(0xffffffffu, exact) && exact) {
+              float amax = -INFINITY;
+#pragma unroll
+              for (int k = 0; k < 32; k += 2) amax = fmax3f(amax, __uint_as_float(v[k]), __uint_as_float(v[k + 1]));
+              const float cmax = __fmul_rn(amax, scale);
+              if (cmax > m) {
+                den = m == -INFINITY ? 0.0 : den * exp(static_cast<double>(m) - static_cast<double>(cmax));
+                m = cmax;
+                ml0 = m * 1.4426950408889634f;
+              }
+              acc = m == -INFINITY ? make_float2(0.f, 0.f) : chunk_sum(ml0);
+            }
+            if (m != -INFINITY) den += static_cast<double>(acc.x) + static_cast<double>(acc.y);
           };
-          float2 acc = make_float2(0.f, 0.f);
-          bool exact = m == -INFINITY;
-          if (!exact) {
-            acc = chunk_sum(ml0);
-            exact = !(acc.x + acc.y <= 256.f);
+          row_chunk(v, m, ml0, den);
+          if (CB_P0G == 2) {  // the second query tile's slice, then the buffer goes back to the MMA
+            tmem_ld32(tl + b * L::SBW + 128, v);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar.s_empty[b]);
+            row_chunk(v, m_1, ml0_1, den_1);
           }
-          if (__any_sync(0xffffffffu, exact) && exact) {
-            float amax = -INFINITY;
-#pragma unroll
-            for (int k = 0; k < 32; k += 2) amax = fmax3f(amax, __uint_as_float(v[k]), __uint_as_float(v[k + 1]));
-            const float cmax = __fmul_rn(amax, scale);
-            if (cmax > m) {
-              den = m == -INFINITY ? 0.0 : den * exp(static_cast<double>(m) - static_cast<double>(cmax));
-              m = cmax;
-              ml0 = m * 1.4426950408889634f;
-            }
-            acc = m == -INFINITY ? make_float2(0.f, 0.f) : chunk_sum(ml0);
-          }
-          if (m != -INFINITY) den += static_cast<double>(acc.x) + static_cast<double>(acc.y);
         } else {
           // columns: the group's queries i = 32w + k; row: key j = c*128 + row.
           float* xy = reinterpret_cast<float*>(smem + L::OFF_XCH) + (sc & 1) * (3 * CB_EW * 128);
@@ -565,28 +583,40 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
         }
       }
       if (PASS == 0) {
-        // merge the column slices of each row: den relative to the common max
-        float* xf = reinterpret_cast<float*>(smem + L::OFF_XCH);
-        double* xd = reinterpret_cast<double*>(smem + L::OFF_XCH + CB_EW * 128 * 4);
-        if (w > 0) {
-          xf[w * 128 + row] = m;
-          xd[w * 128 + row] = den;
+        // merge the column slices of each row: den relative to the common max (per query tile of
+        // the unit, its own exchange area)
+#pragma unroll
+        for (int g = 0; g < CB_P0G; ++g) {
+          float* xf = reinterpret_cast<float*>(smem + L::OFF_XCH + g * CB_EW * 128 * 12);
+          double* xd = reinterpret_cast<double*>(smem + L::OFF_XCH + g * CB_EW * 128 * 12 + CB_EW * 128 * 4);
+          if (w > 0) {
+            xf[w * 128 + row] = g == 0 ? m : m_1;
+            xd[w * 128 + row] = g == 0 ? den : den_1;
+          }
         }
         epi_bar();
         if (w == 0) {
-          float mx = m;
 #pragma unroll
-          for (int o = 1; o < CB_EW; ++o) mx = fmaxf(mx, xf[o * 128 + row]);
-          double tot = m == -INFINITY ? 0.0 : den * exp(static_cast<double>(m) - static_cast<double>(mx));
+          for (int g = 0; g < CB_P0G; ++g) {
+            const float* xf = reinterpret_cast<const float*>(smem + L::OFF_XCH + g * CB_EW * 128 * 12);
+            const double* xd =
+                reinterpret_cast<const double*>(smem + L::OFF_XCH + g * CB_EW * 128 * 12 + CB_EW * 128 * 4);
+            const float mg = g == 0 ? m : m_1;
+            const double dg = g == 0 ? den : den_1;
+            float mx = mg;
 #pragma unroll
-          for (int o = 1; o < CB_EW; ++o) {
-            const float mo = xf[o * 128 + row];
-            if (mo != -INFINITY) tot += xd[o * 128 + row] * exp(static_cast<double>(mo) - static_cast<double>(mx));
-          }
-          const int i = q0 + row;
-          if (i < p.n) {
-            p.row_max[row0 + i] = mx;
-            p.row_rinv[row0 + i] = static_cast<float>(1.0 / tot);
+            for (int o = 1; o < CB_EW; ++o) mx = fmaxf(mx, xf[o * 128 + row]);
+            double tot = mg == -INFINITY ? 0.0 : dg * exp(static_cast<double>(mg) - static_cast<double>(mx));
+#pragma unroll
+            for (int o = 1; o < CB_EW; ++o) {
+              const float mo = xf[o * 128 + row];
+              if (mo != -INFINITY) tot += xd[o * 128 + row] * exp(static_cast<double>(mo) - static_cast<double>(mx));
+            }
+            const int i = q0 + g * BM + row;
+            if (i < p.n) {
+              p.row_max[row0 + i] = mx;
+              p.row_rinv[row0 + i] = static_cast<float>(1.0 / tot);
+            }
           }
         }
       }
@@ -662,7 +692,9 @@ int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s,
   p.row_rinv = rinv;
   p.gmax = gmax;
   p.groups = p.tiles;  // M = 128: one query tile per group
-  rc = D == 64 ? launch_pass<64, 0>(maps, p, st) : launch_pass<128, 0>(maps, p, st);
+  CbParams p0 = p;
+  p0.tiles = (p.tiles + CB_P0G - 1) / CB_P0G;  // units per (b, h): CB_P0G query tiles each
+  rc = D == 64 ? launch_pass<64, 0>(maps, p0, st) : launch_pass<128, 0>(maps, p0, st);
   if (rc == FGA_OK) {
     CbParams p1 = p;
     p1.tiles = (p.groups + CB_P1G - 1) / CB_P1G;  // units per (b, h): CB_P1G groups each
