@@ -84,6 +84,12 @@ constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
 #ifndef FGA_NOEXP
 #define FGA_NOEXP 0  // P = S bits, no exp
 #endif
+#ifndef FGA_PROD_HALF
+#define FGA_PROD_HALF 1  // producers: lanes per 128-byte half row, one key shuffle per row for all its copies
+#endif
+#ifndef FGA_PROD_LPR
+#define FGA_PROD_LPR 8  // FGA_PROD_HALF: lanes per half row (8: 16 bytes each; 4 / 2: 32 / 64 bytes each)
+#endif
 #ifndef FGA_POLY
 #define FGA_POLY 0  // A/B knob: every FGA_POLY-th exp pair on the FMA pipe (0: all on MUFU)
 #endif
@@ -210,7 +216,14 @@ template <int D>
 __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
                                               uint8_t* smem, const Bars& bar, int kv, int part, int lane) {
   using L = WsSmem<D>;
-  constexpr int LPR = D / 8;     // lanes per 2*D-byte row
+  // Lane mapping.  FGA_PROD_HALF: LPR lanes per 128-byte half row (64 columns), 32 / LPR rows per
+  // instruction; each lane copies 16-byte chunks ch, ch + LPR, ... of every half of its row with
+  // the same key (one SHFL per (8 / LPR) * (D / 64) copies; every instruction still covers whole
+  // 32-byte sectors).  Otherwise D/8 lanes cover a whole row (one SHFL per copy).  c2 A/B (min of
+  // 30 flushed launches): whole rows 2.472 ms, 8 lanes per half row 2.400 ms.
+  constexpr int LPR = FGA_PROD_HALF ? FGA_PROD_LPR : D / 8;  // lanes per row (per copy instruction)
+  constexpr int CPL = FGA_PROD_HALF ? 8 / FGA_PROD_LPR : 1;  // chunks per lane per half row
+  constexpr int NH = FGA_PROD_HALF ? D / 64 : 1;             // halves copied per row with one key
   constexpr int RPI = 32 / LPR;  // rows per warp instruction
   constexpr int ROWS = BN / 2;
   const int nslot = kv ? NSV : NSK;
@@ -226,7 +239,7 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
   // SW128 destination: row r's 16-byte chunk cc lands at r*128 + ((cc ^ (r & 7)) << 4).  This
   // lane's rows are mm*RPI + sub (+32i), so (r & 7) cycles with period PER = 8 / RPI in mm and
   // the address is dstb[mm % PER] + compile-time immediate.
-  constexpr int PER = 8 / RPI;
+  constexpr int PER = RPI >= 8 ? 1 : 8 / RPI;
   uint32_t item = 0;
   TileSeq seq(p);
   for (int64_t tile = seq.next(p, bar); tile >= 0; tile = seq.next(p, bar)) {
@@ -260,10 +273,12 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
       const char* src = gsrc;
       // opaque to the optimiser, so src + key * 2D stays one IMAD.WIDE.U32 per copy
       asm volatile("mov.b64 %0, %0;" : "+l"(src));
-      uint32_t dstb[PER];
+      uint32_t dstb[PER][CPL];
 #pragma unroll
       for (int u = 0; u < PER; ++u)
-        dstb[u] = ring_base + slot * L::KV + lane_off + sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
+#pragma unroll
+        for (int x = 0; x < CPL; ++x)
+          dstb[u][x] = ring_base + slot * L::KV + lane_off + sub * 128 + (((cc + LPR * x) ^ ((u * RPI + sub) & 7)) << 4);
       if (FGA_NOGATHER) {
         // timing experiment only: no data movement
       } else if (c * BN + part * ROWS + ROWS <= t.count) {
@@ -272,7 +287,12 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
 #pragma unroll
           for (int mm = 0; mm < 32 / RPI; ++mm) {
             const uint32_t key = static_cast<uint32_t>(__shfl_sync(0xffffffffu, keys[i], mm * RPI + sub));
-            cp_async16_full(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, src + static_cast<size_t>(key) * (D * 2));
+            const char* g = src + static_cast<size_t>(key) * (D * 2);
+#pragma unroll
+            for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+              for (int x = 0; x < CPL; ++x)
+                cp_async16_full(dstb[mm % PER][x] + hh * HALF + (i * 32 + mm * RPI) * 128, g + hh * 128 + x * LPR * 16);
           }
         }
       } else {
@@ -282,7 +302,12 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
           for (int mm = 0; mm < 32 / RPI; ++mm) {
             const int key = __shfl_sync(0xffffffffu, keys[i], mm * RPI + sub);
             const char* g = src + static_cast<size_t>(static_cast<uint32_t>(max(key, 0))) * (D * 2);
-            cp_async16(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, g, key >= 0 ? 16u : 0u);
+#pragma unroll
+            for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+              for (int x = 0; x < CPL; ++x)
+                cp_async16(dstb[mm % PER][x] + hh * HALF + (i * 32 + mm * RPI) * 128, g + hh * 128 + x * LPR * 16,
+                           key >= 0 ? 16u : 0u);
           }
         }
       }
