@@ -43,10 +43,25 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 // Blocking wait with a watchdog: a protocol bug traps (kernel error) after
 // ~2^32 cycles (~2 s) instead of hanging the GPU.
+#ifndef FGA_WAIT_HINT
+#define FGA_WAIT_HINT 0  // A/B knob: suspend-time hint (ns) of the retry try_waits (0: the system default)
+#endif
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity) {
+  if (FGA_WAIT_HINT == 0) return mbar_try_wait(bar, parity);
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "n"(FGA_WAIT_HINT)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try_wait(bar, parity)) {
+  while (!mbar_try_wait_hint(bar, parity)) {
     if (clock64() - t0 > (1ll << 32)) {
 #ifdef FGA_WATCHDOG_PRINT
       if ((threadIdx.x & 31) == 0)
