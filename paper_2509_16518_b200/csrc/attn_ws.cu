@@ -87,9 +87,6 @@ constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
 #ifndef FGA_PROD_HALF
 #define FGA_PROD_HALF 1  // producers: lanes per 128-byte half row, one key shuffle per row for all its copies
 #endif
-#ifndef FGA_PROD_MIX
-#define FGA_PROD_MIX 0  // every producer warp copies 32 rows of K AND the same 32 rows of V of each chunk
-#endif
 #ifndef FGA_PROD_LPR
 #define FGA_PROD_LPR 8  // FGA_PROD_HALF: lanes per half row (8: 16 bytes each; 4 / 2: 32 / 64 bytes each)
 #endif
@@ -100,7 +97,7 @@ constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
 #define FGA_POLY_DEG 3
 #endif
 
-constexpr int FULL_COUNT = FGA_PROD_MIX ? 32 * NPROD : 64;  // cp.async arrivals per K / V ring slot
+constexpr int FULL_COUNT = 64;  // cp.async arrivals per K / V ring slot (two producer warps)
 
 template <int D>
 struct WsSmem {
@@ -317,91 +314,6 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
         }
       }
       cp_async_arrive_noinc(full);
-    }
-  }
-}
-
-// FGA_PROD_MIX: producer warp `part` (0..3, one per SM sub-partition) copies rows
-// 32*part .. 32*part + 31 of both the K and the V chunk, K first (S needs it first), with one key
-// shuffle per row for both.  The four sub-partitions then carry the same copy load at the same
-// point of every chunk; with one ring per warp role (K warps on two sub-partitions, V warps on
-// the other two) the K copies land during the softmax's exp phase on half the sub-partitions
-// only, and the softmax warps there arrived hundreds of cycles after the others (trace).
-template <int D>
-__device__ __forceinline__ void producer_mixed(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
-                                               uint8_t* smem, const Bars& bar, int part, int lane) {
-  using L = WsSmem<D>;
-  constexpr int LPR = 8;            // lanes per 128-byte half row
-  constexpr int NH = D / 64;        // halves per row
-  constexpr int RPI = 32 / LPR;     // rows per instruction
-  constexpr int NI = 32 / RPI;      // instructions (key shuffles) per 32 rows
-  constexpr int PER = 8 / RPI;
-  const uint64_t pol_kv = policy_evict_last();
-  const int sub = lane / LPR, cc = lane % LPR;
-  const uint32_t baseK = smem_u32(smem + L::OFF_K) + part * 32 * 128, baseV = smem_u32(smem + L::OFF_V) + part * 32 * 128;
-  uint32_t item = 0;
-  TileSeq seq(p);
-  for (int64_t tile = seq.next(p, bar); tile >= 0; tile = seq.next(p, bar)) {
-    const Tile t = decode_tile(p, tile);
-    if (part == 0 && lane == 0) report_tile(p, t);
-    const int64_t roff = static_cast<int64_t>(t.row0) * (D * 2) + cc * 16;
-    const char* gk = static_cast<const char*>(p.k) + roff;
-    const char* gv = static_cast<const char*>(p.v) + roff;
-    for (int c = 0; c < t.nchunks; ++c, ++item) {
-      const uint32_t sk = item % NSK, uk = item / NSK, sv = item % NSV, uv = item / NSV;
-      if (p.dense) {  // contiguous keys: TMA boxes from lane 0 of warp 0, everyone else arrives
-        for (int kv = 0; kv < 2; ++kv) {
-          const uint32_t slot = kv ? sv : sk, use = kv ? uv : uk;
-          uint64_t* full = &(kv ? bar.v_full : bar.k_full)[slot];
-          mbar_wait(&(kv ? bar.v_empty : bar.k_empty)[slot], (use & 1) ^ 1);
-          if (part == 0 && lane == 0) {
-            mbar_expect_tx(full, BN * D * 2);
-            uint8_t* ring = smem + (kv ? L::OFF_V : L::OFF_K) + slot * L::KV;
-#pragma unroll
-            for (int h = 0; h < D / 64; ++h)
-              tma_load_2d(ring + h * HALF, kv ? tmV2 : tmK2, full, h * 64, t.row0 + c * BN, pol_kv);
-          } else {
-            mbar_arrive(full);
-          }
-        }
-        continue;
-      }
-      const int r0 = c * BN + part * 32;
-      int key = r0 + lane < t.count ? __ldg(t.list + r0 + lane) : -1;
-      const bool full_rows = r0 + 32 <= t.count;
-      mbar_wait(&bar.k_empty[sk], (uk & 1) ^ 1);
-      key = clamp_key(p, key, r0 + lane < t.count);
-      int kr[NI];  // this lane's row key for each instruction
-#pragma unroll
-      for (int mm = 0; mm < NI; ++mm) kr[mm] = __shfl_sync(0xffffffffu, key, mm * RPI + sub);
-      uint32_t sw[PER];  // SW128: row r's chunk cc at r*128 + ((cc ^ (r & 7)) << 4), r & 7 periodic in mm
-#pragma unroll
-      for (int u = 0; u < PER; ++u) sw[u] = sub * 128 + ((cc ^ ((u * RPI + sub) & 7)) << 4);
-      for (int kv = 0; kv < 2; ++kv) {
-        if (kv == 1) mbar_wait(&bar.v_empty[sv], (uv & 1) ^ 1);
-        const char* src = kv ? gv : gk;
-        asm volatile("mov.b64 %0, %0;" : "+l"(src));  // keep src + key * 2D one IMAD.WIDE per row
-        const uint32_t dst0 = (kv ? baseV + sv * L::KV : baseK + sk * L::KV);
-        if (FGA_NOGATHER) {
-        } else if (full_rows) {
-#pragma unroll
-          for (int mm = 0; mm < NI; ++mm) {
-            const char* g = src + static_cast<size_t>(static_cast<uint32_t>(kr[mm])) * (D * 2);
-#pragma unroll
-            for (int hh = 0; hh < NH; ++hh)
-              cp_async16_full(dst0 + sw[mm % PER] + hh * HALF + mm * RPI * 128, g + hh * 128);
-          }
-        } else {
-#pragma unroll
-          for (int mm = 0; mm < NI; ++mm) {
-            const char* g = src + static_cast<size_t>(static_cast<uint32_t>(max(kr[mm], 0))) * (D * 2);
-#pragma unroll
-            for (int hh = 0; hh < NH; ++hh)
-              cp_async16(dst0 + sw[mm % PER] + hh * HALF + mm * RPI * 128, g + hh * 128, kr[mm] >= 0 ? 16u : 0u);
-          }
-        }
-        cp_async_arrive_noinc(kv ? &bar.v_full[sv] : &bar.k_full[sk]);
-      }
     }
   }
 }
@@ -806,10 +718,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     if (warp < WARP_PROD0) {
       mma_chain<D>(p, smem, bar, tmem, warp - WARP_MMA0);
     } else if (warp < WARP_PROD0 + NPROD) {
-      if (FGA_PROD_MIX)
-        producer_mixed<D>(p, &tmK2, &tmV2, smem, bar, warp - WARP_PROD0, lane);
-      else
-        producer_half<D>(p, &tmK2, &tmV2, smem, bar, (warp - WARP_PROD0) >> 1, (warp - WARP_PROD0) & 1, lane);
+      producer_half<D>(p, &tmK2, &tmV2, smem, bar, (warp - WARP_PROD0) >> 1, (warp - WARP_PROD0) & 1, lane);
     } else if (warp == WARP_SCHED && p.sched != nullptr && lane == 0) {
       tile_scheduler(p, bar);
     }
@@ -858,10 +767,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
   }
   __syncthreads();
   if (warp >= WARP_PROD0 && warp < WARP_PROD0 + NPROD) {
-    if (FGA_PROD_MIX)
-      producer_mixed<D>(p, nullptr, nullptr, smem, bar, warp - WARP_PROD0, lane);
-    else
-      producer_half<D>(p, nullptr, nullptr, smem, bar, (warp - WARP_PROD0) >> 1, (warp - WARP_PROD0) & 1, lane);
+    producer_half<D>(p, nullptr, nullptr, smem, bar, (warp - WARP_PROD0) >> 1, (warp - WARP_PROD0) & 1, lane);
   } else if (warp == 0) {
     const Tile t = decode_tile(p, p.tile_begin);
     for (int c = 0; c < t.nchunks; ++c) {
