@@ -87,6 +87,12 @@ constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
 #ifndef FGA_PROD_HALF
 #define FGA_PROD_HALF 1  // producers: lanes per 128-byte half row, one key shuffle per row for all its copies
 #endif
+#ifndef FGA_KFREE_LATE
+#define FGA_KFREE_LATE 0  // A/B knob: free chunk c's K slot with PV_c's commit instead of S_c's
+#endif
+#ifndef FGA_PROD_SWAP
+#define FGA_PROD_SWAP 0  // A/B knob: 1 puts the K producers on sub-partitions 0/1 and the V producers on 2/3
+#endif
 #ifndef FGA_PROD_LPR
 #define FGA_PROD_LPR 8  // FGA_PROD_HALF: lanes per half row (8: 16 bytes each; 4 / 2: 32 / 64 bytes each)
 #endif
@@ -362,7 +368,7 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
             if (!FGA_NOMMA) umma_ts(tS, tQ + kk * 8, dk + off, IDESC_S, kk > 0 ? 1u : 0u);
           }
           umma_commit(&bar.s_full[r]);
-          umma_commit(&bar.k_empty[slot]);
+          if (!FGA_KFREE_LATE) umma_commit(&bar.k_empty[slot]);
         }
         __syncwarp();
         if (r == 0) FGA_TS(p, it, j, 14);
@@ -392,6 +398,7 @@ __device__ __forceinline__ void mma_chain(const AttnParams& p, uint8_t* smem, co
           for (int kk = 0; kk < BN / 16; ++kk)
             if (!FGA_NOMMA) umma_ts(tO, tS + kk * 8, dv + ((kk * 16 * 128) >> 4), IDESC_O, 1u);
           umma_commit(&bar.v_empty[slot]);
+          if (FGA_KFREE_LATE) umma_commit(&bar.k_empty[c % NSK]);  // S_c is done when PV_c is
           umma_commit(&bar.pv_done[r]);
           mbar_arrive(bar.pv_issued);
         }
@@ -718,7 +725,8 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
     if (warp < WARP_PROD0) {
       mma_chain<D>(p, smem, bar, tmem, warp - WARP_MMA0);
     } else if (warp < WARP_PROD0 + NPROD) {
-      producer_half<D>(p, &tmK2, &tmV2, smem, bar, (warp - WARP_PROD0) >> 1, (warp - WARP_PROD0) & 1, lane);
+      producer_half<D>(p, &tmK2, &tmV2, smem, bar, ((warp - WARP_PROD0) >> 1) ^ FGA_PROD_SWAP, (warp - WARP_PROD0) & 1,
+                       lane);
     } else if (warp == WARP_SCHED && p.sched != nullptr && lane == 0) {
       tile_scheduler(p, bar);
     }
