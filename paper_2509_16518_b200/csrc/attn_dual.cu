@@ -106,7 +106,9 @@ template <int D>
 __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem, const Bars& bar, int kv, int part,
                                               int lane) {
   using L = DuSmem<D>;
-  constexpr int LPR = D / 8, RPI = 32 / LPR, ROWS = BN / 2, PER = 8 / RPI;
+  // 8 lanes per 128-byte half row, each lane copying its 16 bytes of every half of its row with
+  // one key shuffle (attn_ws.cu's producer_half mapping)
+  constexpr int LPR = 8, NH = D / 64, RPI = 32 / LPR, ROWS = BN / 2, PER = 8 / RPI;
   const int nslot = kv ? NSV : NSK;
   const int sub = lane / LPR, ch = lane % LPR;
   const uint32_t lane_off = static_cast<uint32_t>((ch >> 3) * HALF);
@@ -147,7 +149,10 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem
 #pragma unroll
           for (int mm = 0; mm < 32 / RPI; ++mm) {
             const uint32_t key = static_cast<uint32_t>(__shfl_sync(0xffffffffu, keys[i], mm * RPI + sub));
-            cp_async16_full(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, src + static_cast<size_t>(key) * (D * 2));
+            const char* g = src + static_cast<size_t>(key) * (D * 2);
+#pragma unroll
+            for (int hh = 0; hh < NH; ++hh)
+              cp_async16_full(dstb[mm % PER] + hh * HALF + (i * 32 + mm * RPI) * 128, g + hh * 128);
           }
         }
       } else {
@@ -157,7 +162,9 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, uint8_t* smem
           for (int mm = 0; mm < 32 / RPI; ++mm) {
             const int key = __shfl_sync(0xffffffffu, keys[i], mm * RPI + sub);
             const char* g = src + static_cast<size_t>(static_cast<uint32_t>(max(key, 0))) * (D * 2);
-            cp_async16(dstb[mm % PER] + (i * 32 + mm * RPI) * 128, g, key >= 0 ? 16u : 0u);
+#pragma unroll
+            for (int hh = 0; hh < NH; ++hh)
+              cp_async16(dstb[mm % PER] + hh * HALF + (i * 32 + mm * RPI) * 128, g + hh * 128, key >= 0 ? 16u : 0u);
           }
         }
       }
