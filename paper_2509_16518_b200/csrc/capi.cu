@@ -355,8 +355,8 @@ int fga_build_mask_avgq(const void* q, const void* k, fga_shape shape, int strat
     out.fill = fill_sentinel;
     if (out.keep_bits == nullptr || out.fix_rows == nullptr || out.fix_count == nullptr)
       return fail(FGA_EINVAL, "build_mask_avgq: workspace too small (fga_workspace_bytes)");
-    if (cudaMemsetAsync(out.fix_count, 0, sizeof(int32_t), st) != cudaSuccess) return check_launch("memset");
-    return launch_pooled_scores(q, k, shape, 1, out, w, st);  // scores -> keep bits -> lists -> argmax fix-up
+    // (fix_count is zeroed by the pooled-mean launch) scores -> keep bits -> lists -> argmax fix-up
+    return launch_pooled_scores(q, k, shape, 1, out, w, st);
   }
   if (round_bf16 && n <= FGA_SELECT_MAX_N) {  // bf16 scores -> fused selection + compaction
     Workspace pw = w;

@@ -44,10 +44,13 @@ __global__ void pooled_mean_kernel(const __nv_bfloat16* __restrict__ q, float* _
 // M x D bf16 block -- brought into shared memory by TMA bulk copies first: one CTA of D threads
 // per group, thread = column.  Used when the block is 16-byte aligned and fits in 64 KB.  With
 // parts != null it also writes the three bf16 parts of q̄ the tensor-core score pass reads
-// (split3_kernel's split, parts_n = B*H*G*D elements per part).
+// (split3_kernel's split, parts_n = B*H*G*D elements per part).  zero_word (nullable) is set to 0
+// by block 0 (the fused threshold's empty-row counter, instead of a separate memset).
 constexpr int PM_MAX_BYTES = 64 * 1024;
 __global__ void pooled_mean_bulk_kernel(const __nv_bfloat16* __restrict__ q, float* __restrict__ qbar, int N, int D,
-                                        int M, int G, __nv_bfloat16* __restrict__ parts, int64_t parts_n) {
+                                        int M, int G, __nv_bfloat16* __restrict__ parts, int64_t parts_n,
+                                        int32_t* __restrict__ zero_word) {
+  if (zero_word != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *zero_word = 0;
   extern __shared__ __align__(16) __nv_bfloat16 s_rows[];
   __shared__ __align__(8) uint64_t bar;
   const int64_t bhg = blockIdx.x;
@@ -541,9 +544,12 @@ int launch_pooled_scores(const void* q, const void* k, const fga_shape& s, int r
       return rc;
     pooled_mean_bulk_kernel<<<static_cast<unsigned>(B * H * G), static_cast<unsigned>(D), static_cast<size_t>(blk),
                               st>>>(static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N),
-                                    static_cast<int>(D), static_cast<int>(M), static_cast<int>(G), parts, B * H * G * D);
+                                    static_cast<int>(D), static_cast<int>(M), static_cast<int>(G), parts, B * H * G * D,
+                                    out.fix_count);
     parts_ready = true;
   } else {
+    if (out.fix_count != nullptr && cudaMemsetAsync(out.fix_count, 0, sizeof(int32_t), st) != cudaSuccess)
+      return check_launch("memset");
     pooled_mean_kernel<<<static_cast<unsigned>(B * H * G), 128, 0, st>>>(
         static_cast<const __nv_bfloat16*>(q), qbar, static_cast<int>(N), static_cast<int>(D), static_cast<int>(M),
         static_cast<int>(G));
