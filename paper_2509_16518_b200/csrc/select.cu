@@ -65,7 +65,7 @@ template <bool TOPK>
 __global__ void __launch_bounds__(SEL_THREADS, 2)
     select_compact_kernel(const uint16_t* __restrict__ scores, int64_t n64, float tau, int64_t top_k,
                           int32_t* __restrict__ idx, int64_t stride, int32_t* __restrict__ counts, int fill) {
-  extern __shared__ __align__(16) uint16_t s_key[];  // the row's bf16 bits, padded with -NaN to a multiple of 8
+  extern __shared__ __align__(16) uint16_t s_key[];  // the row's bf16 bits, padded with -NaN to a multiple of 256
   __shared__ int s_red[2 * SEL_WARPS];
   __shared__ int s_cnt[2][SEL_WARPS];
   __shared__ unsigned long long s_best[SEL_WARPS];
@@ -76,7 +76,9 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
   const uint16_t* src = scores + row * n64;
   int32_t* out = idx + row * stride;
   const int nv = (n + 7) / 8;  // 16-byte vectors of keys
+  const int nvp = (nv + 31) / 32 * 32;  // padded to whole 256-key blocks: the block loops need no bound check
   uint4* sv = reinterpret_cast<uint4*>(s_key);
+  for (int i = nv + tid; i < nvp; i += SEL_THREADS) sv[i] = make_uint4(~0u, ~0u, ~0u, ~0u);  // -NaN: never counted
 
   // ---- 1. load (+ range of the order-preserving keys for the bisection)
   uint32_t kmin2 = 0xFFFFFFFFu, kmax2 = 0u;
@@ -150,14 +152,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
       const __nv_bfloat162 piv = *reinterpret_cast<const __nv_bfloat162*>(&pb);
       uint32_t acc = 0;  // two 16-bit counters of -1s (|count| <= n/16 per thread each)
       for (int b = b0; b < b1; ++b) {
-        const int vi = b * 32 + lane;
-        if (vi < nv) {
-          const uint4 x = sv[vi];
-          acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.x), piv));
-          acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.y), piv));
-          acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.z), piv));
-          acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.w), piv));
-        }
+        const uint4 x = sv[b * 32 + lane];
+        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.x), piv));
+        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.y), piv));
+        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.z), piv));
+        acc = __vadd2(acc, __hge2_mask(*reinterpret_cast<const __nv_bfloat162*>(&x.w), piv));
       }
       const int mine = static_cast<int>(((0x10000u - (acc & 0xFFFFu)) & 0xFFFFu) + ((0x10000u - (acc >> 16)) & 0xFFFFu));
       return __reduce_add_sync(0xffffffffu, mine);
@@ -174,9 +173,9 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
     int c_lo = n, c_hi1 = 0;  // block-wide #{s >= value(lo)} (every non-NaN key at kmin), #{s >= value(hi + 1)}
     while (lo < hi) {  // block-uniform
       uint32_t mid = (lo + hi + 1) >> 1;
-      if (interp && c_lo > c_hi1) {
-        const uint32_t span = hi + 1 - lo;
-        const uint32_t step = static_cast<uint32_t>(static_cast<uint64_t>(c_lo - k) * span / static_cast<uint64_t>(c_lo - c_hi1));
+      if (interp && c_lo > c_hi1) {  // (a heuristic pivot: float arithmetic is plenty)
+        const float span = static_cast<float>(hi + 1 - lo);
+        const uint32_t step = static_cast<uint32_t>(static_cast<float>(c_lo - k) * span / static_cast<float>(c_lo - c_hi1));
         mid = lo + min(max(step, 1u), hi - lo);
       }
       const int wc = count_ge(mid);
@@ -205,7 +204,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
     uint32_t ga = 0;
     for (int b = b0; b < b1; ++b) {
       const int vi = b * 32 + lane;
-      if (vi < nv) {
+      if (vi < nv) {  // (measured faster than the unguarded loop here, unlike the top-k passes)
         const uint4 x = sv[vi];
         const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -245,8 +244,8 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
   //      are its above-cut keys plus its lowest few ties, written at consecutive positions.
   for (int b = b0; b < b1; ++b) {
     const int vi = b * 32 + lane;
-    uint32_t gm = 0, em = 0;  // bit j: key 8*vi + j
-    if (vi < nv) {
+    uint32_t gm = 0, em = 0;  // bit j: key 8*vi + j (the -NaN padding never holds)
+    if (TOPK || vi < nv) {
       const uint4 x = sv[vi];
       const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -337,7 +336,7 @@ int launch_select_compact(const uint16_t* scores, int64_t rows, int64_t n, int m
   if (mode == FGA_SELECT_TOPK && (top_k < 1 || top_k > n)) return fail(FGA_EINVAL, "top_k must be in [1, n]");
   if (rows == 0) return FGA_OK;
   if (rows >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "select_compact: too many rows");
-  const int smem = static_cast<int>(((n + 7) / 8) * 16);
+  const int smem = static_cast<int>(((n + 7) / 8 + 31) / 32 * 32 * 16);  // whole 256-key blocks
   int rc;
   if (mode == FGA_SELECT_TOPK) {
     if ((rc = smem_opt_in(reinterpret_cast<const void*>(select_compact_kernel<true>), smem, "select_compact")) != FGA_OK)
