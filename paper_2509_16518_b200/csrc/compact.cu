@@ -28,7 +28,10 @@
 // issue-slot utilisation, 3.2 TB/s — ~270 instructions of per-round overhead
 // per warp; one warp per row removed the barriers but left one serial step
 // chain per warp with ~21 warps per SM: 2.5 TB/s.)
+#include <type_traits>
+
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace fga {
 namespace {
@@ -45,6 +48,9 @@ constexpr int STEP = 1024;  // keys per warp step
 #endif
 #ifndef FGA_CK_BUFS
 #define FGA_CK_BUFS 1
+#endif
+#ifndef FGA_CK_BULK
+#define FGA_CK_BULK 1  // stage absolute int32 keys and write each step's aligned body with one TMA bulk store
 #endif
 constexpr int WARPS = FGA_CK_WARPS;
 constexpr int SPW = FGA_CK_SPW;    // steps per warp per round: 8 x 4 steps = 32768 keys (c2's whole row)
@@ -64,6 +70,13 @@ __device__ __forceinline__ void emit16(uint16_t* st, int off, uint32_t m, int re
 #pragma unroll
   for (int e = 0; e < 16; ++e)
     if (m & (1u << e)) st[off++] = static_cast<uint16_t>(rel0 + e);
+}
+
+// the same for an int32 stage of absolute keys v0 + e
+__device__ __forceinline__ void emit16_i32(int32_t* st, int off, uint32_t m, int v0) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+    if (m & (1u << e)) st[off++] = v0 + e;
 }
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -133,11 +146,21 @@ struct BitSrc {
   __device__ __forceinline__ int key_base(int64_t s) const { return static_cast<int>(s * STEP); }
 };
 
+// Stage element: uint16 positions relative to the step (flushed by coalesced stores), or with
+// FGA_CK_BULK int32 absolute keys placed at (output position) mod 4, so that the step's run
+// out[base .. base + tot) splits into <= 3 head keys, a 16-byte-aligned body written from shared
+// memory by one `cp.async.bulk` (TMA) store, and <= 3 tail keys -- the per-key flush loads and
+// stores (~10 instructions per 32 keys with their address arithmetic) become one instruction per step.
+constexpr int STAGE_N = FGA_CK_BULK ? STEP + 4 : STEP;
+using StageT = typename std::conditional<FGA_CK_BULK, int32_t, uint16_t>::type;
+
 template <class Src>
 __device__ __forceinline__ int compact_row(const Src& src, int64_t nsteps, int32_t* __restrict__ out,
-                                           int (*s_warp)[WARPS], uint16_t (*stage)[STEP]) {
+                                           int (*s_warp)[WARPS], StageT (*stage)[STAGE_N]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int running = 0, rb = 0;
+  const bool bulk = FGA_CK_BULK && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  bool pending = false;  // lane 0: a bulk store may still be reading this warp's stage
   for (int64_t r0 = 0; r0 < nsteps; r0 += WARPS * SPW, rb ^= 1) {
     const int64_t s0 = r0 + int64_t(warp) * SPW;
     decltype(src.load(0)) d[SPW];
@@ -177,17 +200,41 @@ __device__ __forceinline__ int compact_row(const Src& src, int64_t nsteps, int32
     const int rel0 = Src::kHalfMajor ? lane * 16 : lane * 32;
 #pragma unroll
     for (int j = 0; j < SPW; ++j) {
-      uint16_t* st = stage[warp * BUFS + (j % BUFS)];
-      if (BUFS == 1 && j > 0) __syncwarp();  // the previous step's flush has read the stage
-      emit16(st, o0[j], m0[j], rel0);
-      emit16(st, o1[j], m1[j], rel1);
-      __syncwarp();
+      StageT* st = stage[warp * BUFS + (j % BUFS)];
       const int kb = src.key_base(s0 + j);
-      for (int i = lane; i < tot[j]; i += 32) out[base + i] = kb + st[i];
+      if constexpr (FGA_CK_BULK) {
+        if (lane == 0 && pending) bulk_wait_read_all();  // the previous step's bulk store has read the stage
+        __syncwarp();
+        const int shift = base & 3, tj = tot[j];
+        emit16_i32(st + shift, o0[j], m0[j], kb + rel0);
+        emit16_i32(st + shift, o1[j], m1[j], kb + rel1);
+        if (bulk) fence_proxy_async_smem();  // the stage's generic-proxy writes -> the bulk store
+        __syncwarp();
+        const int i0 = bulk ? min(tj, (4 - shift) & 3) : tj;  // aligned body [i0, i1)
+        const int i1 = bulk ? i0 + ((tj - i0) & ~3) : tj;
+        if (!bulk) {
+          for (int i = lane; i < tj; i += 32) out[base + i] = st[shift + i];
+        } else {
+          if (lane < i0) out[base + lane] = st[shift + lane];
+          if (lane < tj - i1) out[base + i1 + lane] = st[shift + i1 + lane];
+          if (lane == 0 && i1 > i0) {
+            bulk_s2g(out + base + i0, st + shift + i0, static_cast<uint32_t>(i1 - i0) * 4u);
+            bulk_commit();
+            pending = true;
+          }
+        }
+      } else {
+        if (BUFS == 1 && j > 0) __syncwarp();  // the previous step's flush has read the stage
+        emit16(reinterpret_cast<uint16_t*>(st), o0[j], m0[j], rel0);
+        emit16(reinterpret_cast<uint16_t*>(st), o1[j], m1[j], rel1);
+        __syncwarp();
+        for (int i = lane; i < tot[j]; i += 32) out[base + i] = kb + reinterpret_cast<uint16_t*>(st)[i];
+      }
       base += tot[j];
     }
     running += rtotal;
   }
+  if (FGA_CK_BULK && lane == 0 && pending) bulk_wait_all();  // stores complete before the CTA exits
   return running;
 }
 
@@ -198,7 +245,7 @@ __global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_kernel(co
   __shared__ int s_warp[2][WARPS];
   __shared__ float s_bv[WARPS];
   __shared__ int s_bi[WARPS];
-  __shared__ uint16_t s_stage[WARPS * BUFS][STEP];
+  __shared__ __align__(16) StageT s_stage[WARPS * BUFS][STAGE_N];
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint8_t* kr = keep + row * n;
@@ -260,7 +307,7 @@ __global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_bits_kern
                                                                      int fill, int32_t* __restrict__ fix_rows,
                                                                      int32_t* __restrict__ fix_count) {
   __shared__ int s_warp[2][WARPS];
-  __shared__ uint16_t s_stage[WARPS * BUFS][STEP];
+  __shared__ __align__(16) StageT s_stage[WARPS * BUFS][STAGE_N];
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x;
   int32_t* out = idx + row * stride;
