@@ -52,6 +52,9 @@ constexpr int CB_P1G = 1;  // pass 1: groups per unit (the exact-select variant 
 #else
 constexpr int CB_P1G = 2;  // pass 1: two groups per unit share every K chunk (half the L2 -> SMEM bytes)
 #endif
+#ifndef FGA_CB_P1N256
+#define FGA_CB_P1N256 1  // pass 1: the unit's two group tiles as one N = 256 MMA per K step
+#endif
 #ifndef FGA_CB_P0G
 #define FGA_CB_P0G 1  // 2 measured slower: 3.6 -> 4.2 ms (bitwise the same output)
 #endif
@@ -158,6 +161,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
   // with a key chunk range.  Passes 0 (row statistics over every key) and 3 stride over whole units.
   constexpr bool FLAT = PASS == 1 || PASS == 2;
   const int64_t flat_n = p.bh * p.tiles * static_cast<int64_t>(p.nch);
+  constexpr bool P1W = PASS == 1 && CB_P1G == 2 && FGA_CB_P1N256;  // pass 1 as N = 256 MMAs
   struct Seq {
     int64_t u, f, hi;
   };
@@ -229,7 +233,10 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
                                      : row0 + (t * L::NQ + qp) * BM;  // pass 1: group CB_P1G*t + qp
 #pragma unroll
           for (int h = 0; h < D / 64; ++h)
-            tma_load_2d(smem + L::OFF_Q + qp * L::KV + h * HALF, &tmQ, bar.q_full, h * 64, qrow, pol_q);
+            // (pass 1 with N = 256: the groups' tiles interleaved per 64-column half, so each half
+            // holds 256 consecutive rows for one B descriptor)
+            tma_load_2d(smem + L::OFF_Q + (P1W ? h * L::NQ * HALF + qp * HALF : qp * L::KV + h * HALF), &tmQ,
+                        bar.q_full, h * 64, qrow, pol_q);
         }
         for (int c = c_lo; c < c_hi; ++c, ++kc) {
           const uint32_t slot = kc % L::NS, use = kc / L::NS;
@@ -260,7 +267,20 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
         mbar_wait(&bar.s_empty[b], ((sc / L::NSB) & 1) ^ 1);
         tc_fence_after();
         const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
-        if (elect_one()) {
+        if (P1W) {
+          if (elect_one()) {
+            constexpr uint32_t IDESC_W = idesc_bf16(BM, 2 * BN, false, false);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t off = ((kk >> 2) * HALF + (kk & 3) * 32) >> 4;
+              const uint32_t offq = ((kk >> 2) * 2 * HALF + (kk & 3) * 32) >> 4;
+              umma_ss(tmem + b * L::SBW, dk + off, dq0 + offq, IDESC_W, kk > 0 ? 1u : 0u);
+            }
+            umma_commit(&bar.s_full[b]);
+            umma_commit(&bar.k_empty[slot]);
+            if (c == c_hi - 1) umma_commit(bar.q_empty);
+          }
+        } else if (elect_one()) {
 #pragma unroll
           for (int qp = 0; qp < L::NQ; ++qp) {  // pass 2: S^T = K (q̄_hi + q̄_mid + q̄_lo)^T, exact splits
 #pragma unroll
