@@ -47,6 +47,17 @@ __device__ __forceinline__ uint32_t okey_bits(uint32_t k) {  // inverse of okey2
   return (k & 0x8000u) ? (k & 0x7FFFu) : (~k & 0xFFFFu);
 }
 __device__ __forceinline__ float bf16_value(uint32_t b) { return __uint_as_float(b << 16); }
+#ifndef FGA_SEL_HMASK
+#define FGA_SEL_HMASK 1  // emission masks from bf16x2 compares (HSET2) packed to 8 bits
+#endif
+// four bf16x2 compare masks (0xFFFF per half that holds; m_j: keys 2j low, 2j + 1 high) -> bit i = key i
+__device__ __forceinline__ uint32_t pack8(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
+  const uint32_t t = (m0 & 0x00020001u) | (m1 & 0x00080004u) | (m2 & 0x00200010u) | (m3 & 0x00800040u);
+  return (t | (t >> 16)) & 0xFFu;
+}
+__device__ __forceinline__ const __nv_bfloat162& as_b2(const uint32_t& w) {
+  return *reinterpret_cast<const __nv_bfloat162*>(&w);
+}
 
 // sum over the block of the warps' partial sums (v: this warp's, the same in every lane); `red`
 // holds two buffers of SEL_WARPS (the phase alternates, so one barrier per call suffices)
@@ -242,10 +253,24 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
   // ---- 4. emit, ascending: per 256-key block one packed warp scan of (kept-above, ties) counts;
   //      the ties kept before lane l are min(tie prefix, ties still needed), so a lane's kept keys
   //      are its above-cut keys plus its lowest few ties, written at consecutive positions.
+  const uint32_t thr2b = __bfloat16_as_ushort(__float2bfloat16_rn(thr)) * 0x00010001u;  // thr is a bf16 value
+  const uint32_t tau2b = __bfloat16_as_ushort(__float2bfloat16_ru(tau)) * 0x00010001u;
+  const __nv_bfloat162 thr2 = as_b2(thr2b), tau2 = as_b2(tau2b);
   for (int b = b0; b < b1; ++b) {
     const int vi = b * 32 + lane;
     uint32_t gm = 0, em = 0;  // bit j: key 8*vi + j (the -NaN padding never holds)
-    if (TOPK || vi < nv) {
+    if (FGA_SEL_HMASK && (TOPK || vi < nv)) {
+      const uint4 x = sv[vi];
+      if (TOPK) {
+        gm = pack8(__hgt2_mask(as_b2(x.x), thr2), __hgt2_mask(as_b2(x.y), thr2), __hgt2_mask(as_b2(x.z), thr2),
+                   __hgt2_mask(as_b2(x.w), thr2));
+        em = pack8(__heq2_mask(as_b2(x.x), thr2), __heq2_mask(as_b2(x.y), thr2), __heq2_mask(as_b2(x.z), thr2),
+                   __heq2_mask(as_b2(x.w), thr2));
+      } else {
+        gm = pack8(__hge2_mask(as_b2(x.x), tau2), __hge2_mask(as_b2(x.y), tau2), __hge2_mask(as_b2(x.z), tau2),
+                   __hge2_mask(as_b2(x.w), tau2));
+      }
+    } else if (TOPK || vi < nv) {
       const uint4 x = sv[vi];
       const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
