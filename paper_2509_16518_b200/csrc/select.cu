@@ -256,6 +256,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
   const uint32_t thr2b = __bfloat16_as_ushort(__float2bfloat16_rn(thr)) * 0x00010001u;  // thr is a bf16 value
   const uint32_t tau2b = __bfloat16_as_ushort(__float2bfloat16_ru(tau)) * 0x00010001u;
   const __nv_bfloat162 thr2 = as_b2(thr2b), tau2 = as_b2(tau2b);
+#ifndef FGA_SEL_OUTREG
+#define FGA_SEL_OUTREG 1  // keep the row's output pointer in a register (no per-store rematerialisation)
+#endif
+  int32_t* outr = out;
+  if (FGA_SEL_OUTREG && TOPK) asm volatile("mov.b64 %0, %0;" : "+l"(outr));  // (threshold: measured slower)
   for (int b = b0; b < b1; ++b) {
     const int vi = b * 32 + lane;
     uint32_t gm = 0, em = 0;  // bit j: key 8*vi + j (the -NaN padding never holds)
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 2)
     }
     // a running output pointer stepped by the keep bit: predicated stores, no per-slot address
     // arithmetic or branch
-    int32_t* op = out + at;
+    int32_t* op = outr + at;
     const int key0 = vi * 8;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
