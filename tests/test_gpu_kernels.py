@@ -120,6 +120,37 @@ def test_compact_bit_exact(n, fill):
             assert (got[r, c[r]:] == 12345).all()
 
 
+@pytest.mark.parametrize("n", [31, 1000, 32760, 40001])
+@pytest.mark.parametrize("pad", [0, 1, 4])
+@pytest.mark.parametrize("fill", [0, 1])
+def test_compact_bits_strides(n, pad, fill):
+    # bit-packed compaction into rows of stride n + pad: 16-byte aligned rows take the TMA bulk-store
+    # flush (head / body / tail split at the output position mod 4), the others the per-key stores;
+    # nothing is written past the count without the -1 fill, nothing past n with it
+    rng = np.random.default_rng(n + pad)
+    rows = 29
+    keep = (rng.random((rows, n)) < rng.random((rows, 1))).astype(np.uint8)
+    keep[2] = 0
+    keep[3] = 1
+    kd = torch.from_numpy(keep).cuda()
+    words = (n + 31) // 32
+    bits = torch.empty((rows, words), dtype=torch.int32, device="cuda")
+    _lib.call("fga_pack_bits", ptr(kd), rows, n, ptr(bits), stream())
+    stride = n + pad
+    idx = torch.full((rows, stride), 12345, dtype=torch.int32, device="cuda")
+    cnt = torch.empty(rows, dtype=torch.int32, device="cuda")
+    _lib.call("fga_compact_bits", ptr(bits), rows, n, ptr(idx), stride, ptr(cnt), fill, stream())
+    torch.cuda.synchronize()
+    got, c = idx.cpu().numpy(), cnt.cpu().numpy()
+    for r in range(rows):
+        pos = np.flatnonzero(keep[r])
+        assert c[r] == pos.size, r
+        assert np.array_equal(got[r, : c[r]], pos), r
+        tail = got[r, c[r]:n]
+        assert ((tail == -1) if fill else (tail == 12345)).all(), r
+        assert (got[r, n:] == 12345).all(), r
+
+
 def test_compact_unaligned_rows_without_scores():
     # row starts at odd byte offsets (n = 13) and no fallback: empty rows keep count 0
     rng = np.random.default_rng(1)
