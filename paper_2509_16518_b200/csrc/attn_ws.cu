@@ -90,6 +90,9 @@ constexpr uint32_t TM_O = 0, TM_Q = 128, TM_S = 256;
 #ifndef FGA_KFREE_LATE
 #define FGA_KFREE_LATE 0  // A/B knob: free chunk c's K slot with PV_c's commit instead of S_c's
 #endif
+#ifndef FGA_QPF
+#define FGA_QPF 1  // the first producer prefetches each tile's Q rows into L2 when it starts the tile
+#endif
 #ifndef FGA_PROD_SWAP
 #define FGA_PROD_SWAP 0  // A/B knob: 1 puts the K producers on sub-partitions 0/1 and the V producers on 2/3
 #endif
@@ -222,7 +225,8 @@ __device__ __forceinline__ void tile_scheduler(const AttnParams& p, const Bars& 
 // so no stale or NaN bytes reach the MMA.
 template <int D>
 __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtensorMap* tmK2, const CUtensorMap* tmV2,
-                                              uint8_t* smem, const Bars& bar, int kv, int part, int lane) {
+                                              uint8_t* smem, const Bars& bar, int kv, int part, int lane,
+                                              const void* qptr = nullptr) {
   using L = WsSmem<D>;
   // Lane mapping.  FGA_PROD_HALF: LPR lanes per 128-byte half row (64 columns), 32 / LPR rows per
   // instruction; each lane copies 16-byte chunks ch, ch + LPR, ... of every half of its row with
@@ -252,7 +256,14 @@ __device__ __forceinline__ void producer_half(const AttnParams& p, const CUtenso
   TileSeq seq(p);
   for (int64_t tile = seq.next(p, bar); tile >= 0; tile = seq.next(p, bar)) {
     const Tile t = decode_tile(p, tile);
-    if (kv == 0 && part == 0 && lane == 0) report_tile(p, t);
+    if (kv == 0 && part == 0 && lane == 0) {
+      report_tile(p, t);
+      // the producers start a tile ~3 chunks before the softmax warps load its Q rows
+      // (write_q at the end of the previous tile): have them in L2 by then
+      if (FGA_QPF && qptr != nullptr)
+        bulk_prefetch_l2(static_cast<const __nv_bfloat16*>(qptr) + (static_cast<int64_t>(t.row0) + t.q0) * D,
+                         static_cast<uint32_t>(t.rows) * D * 2);
+    }
     const char* gsrc = static_cast<const char*>(kv ? p.v : p.k) + static_cast<int64_t>(t.row0) * (D * 2) + ch * 16;
     for (int c = 0; c < t.nchunks; ++c, ++item) {
       const uint32_t slot = item % nslot, use = item / nslot;
@@ -726,7 +737,7 @@ __global__ void __launch_bounds__(32 * NWARPS, 1)
       mma_chain<D>(p, smem, bar, tmem, warp - WARP_MMA0);
     } else if (warp < WARP_PROD0 + NPROD) {
       producer_half<D>(p, &tmK2, &tmV2, smem, bar, ((warp - WARP_PROD0) >> 1) ^ FGA_PROD_SWAP, (warp - WARP_PROD0) & 1,
-                       lane);
+                       lane, qptr);
     } else if (warp == WARP_SCHED && p.sched != nullptr && lane == 0) {
       tile_scheduler(p, bar);
     }
