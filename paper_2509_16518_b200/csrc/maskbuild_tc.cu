@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -127,8 +128,15 @@ struct CbParams {
   float* row_max;  // [B*H*N]
   float* row_rinv; // [B*H*N]
   float* gmax;     // [B*H*G*N]
+  long long* dbg;  // FGA_CB_TRACE builds: clock64 timeline of CTA 0's first 256 chunks (pass 0)
 };
 
+#ifdef FGA_CB_TRACE
+#define CB_TS(kc, slot_) \
+  do { if (PASS == 0 && p.dbg != nullptr && blockIdx.x == 0 && (kc) < 256) p.dbg[(kc) * 8 + (slot_)] = clock64(); } while (0)
+#else
+#define CB_TS(kc, slot_) do { } while (0)
+#endif
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * CB_EPI) : "memory"); }
 
 template <int D, int PASS>
@@ -240,7 +248,9 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
         }
         for (int c = c_lo; c < c_hi; ++c, ++kc) {
           const uint32_t slot = kc % L::NS, use = kc / L::NS;
+          CB_TS(kc, 0);
           mbar_wait(&bar.k_empty[slot], (use & 1) ^ 1);
+          CB_TS(kc, 1);
           mbar_expect_tx(&bar.k_full[slot], BN * D * 2);
 #pragma unroll
           for (int h = 0; h < D / 64; ++h)
@@ -263,8 +273,11 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       mbar_wait(bar.q_full, it & 1);
       for (int c = c_lo; c < c_hi; ++c, ++kc, ++sc) {
         const uint32_t slot = kc % L::NS, use = kc / L::NS, b = sc % L::NSB;
+        CB_TS(kc, 2);
         mbar_wait(&bar.k_full[slot], use & 1);
+        CB_TS(kc, 3);
         mbar_wait(&bar.s_empty[b], ((sc / L::NSB) & 1) ^ 1);
+        CB_TS(kc, 4);
         tc_fence_after();
         const uint64_t dk = dk0 + ((slot * L::KV) >> 4);
         if (P1W) {
@@ -361,7 +374,9 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
       uint32_t best_rank = 0, best_j = 0xFFFFFFFFu;
       for (int c = c_lo; c < c_hi; ++c, ++sc) {
         const uint32_t b = sc % L::NSB;
+        if (tid == 0) CB_TS(sc, 5);
         mbar_wait(&bar.s_full[b], (sc / L::NSB) & 1);
+        if (tid == 0) CB_TS(sc, 6);
         tc_fence_after();
         if constexpr (PASS == 3) {
           // exact score of key j for the row's group (the fused pass's arithmetic), running argmax:
@@ -505,6 +520,7 @@ __global__ void __launch_bounds__(32 * CB_WARPS, 1)
             if (m != -INFINITY) den += static_cast<double>(acc.x) + static_cast<double>(acc.y);
           };
           row_chunk(v, m, ml0, den);
+          if (tid == 0) CB_TS(sc, 7);
           if (CB_P0G == 2) {  // the second query tile's slice, then the buffer goes back to the MMA
             tmem_ld32(tl + b * L::SBW + 128, v);
             tmem_ld_wait();
@@ -702,6 +718,12 @@ int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s,
   if ((rc = make_tmap_bf16_2d(&maps[0], q, rows, D, 64, BM)) != FGA_OK) return rc;
   if ((rc = make_tmap_bf16_2d(&maps[1], k, rows, D, 64, BN)) != FGA_OK) return rc;
   CbParams p{};
+#ifdef FGA_CB_TRACE
+  static long long* dbg = nullptr;
+  if (dbg == nullptr) cudaMalloc(&dbg, 256 * 8 * sizeof(long long));
+  cudaMemsetAsync(dbg, 0, 256 * 8 * sizeof(long long), st);
+  p.dbg = dbg;
+#endif
   p.bh = B * H;
   p.n = static_cast<int>(N);
   p.tiles = static_cast<int>((N + BM - 1) / BM);
@@ -715,6 +737,20 @@ int launch_cached_group_max_tc(const void* q, const void* k, const fga_shape& s,
   CbParams p0 = p;
   p0.tiles = (p.tiles + CB_P0G - 1) / CB_P0G;  // units per (b, h): CB_P0G query tiles each
   rc = D == 64 ? launch_pass<64, 0>(maps, p0, st) : launch_pass<128, 0>(maps, p0, st);
+#ifdef FGA_CB_TRACE
+  if (const char* f = std::getenv("FGA_CB_TRACE_FILE")) {
+    long long host[256 * 8];
+    cudaMemcpyAsync(host, p.dbg, sizeof(host), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE* fp = std::fopen(f, "w")) {
+      for (int i = 0; i < 256; ++i) {
+        for (int j = 0; j < 8; ++j) std::fprintf(fp, "%lld ", host[i * 8 + j]);
+        std::fprintf(fp, "\n");
+      }
+      std::fclose(fp);
+    }
+  }
+#endif
   if (rc == FGA_OK) {
     CbParams p1 = p;
     p1.tiles = (p.groups + CB_P1G - 1) / CB_P1G;  // units per (b, h): CB_P1G groups each
