@@ -255,3 +255,23 @@ def test_fused_threshold_band_edges(mode, monkeypatch):
     assert torch.equal(me.counts, m.counts)
     assert all(torch.equal(me.idx.view(counts.size, -1)[r, :c], m.idx.view(counts.size, -1)[r, :c])
                for r, c in enumerate(counts.tolist()))
+
+
+@pytest.mark.parametrize("gain", [8.0, 60.0])
+def test_fused_threshold_extreme_scores(gain):
+    # large query / key magnitudes: scores overflow to inf (kept when tau is finite) or underflow to
+    # 0; the accumulator compare and the exact band must agree with the selection on the same scores
+    n, d = 2000, 64
+    cfg = fga.AttnConfig(1, 2, n, d, precision="bf16")
+    g = torch.Generator(device="cuda").manual_seed(int(gain))
+    q = (torch.randn(cfg.dims, device="cuda", generator=g) * gain).to(torch.bfloat16)
+    k = (torch.randn(cfg.dims, device="cuda", generator=g) * gain).to(torch.bfloat16)
+    rows = fga.pooled_query_scores(q, k, cfg).cpu().numpy().reshape(-1, n)
+    finite = rows[np.isfinite(rows)]
+    for tau in (float(np.quantile(finite, 0.5)) or 1e-3, 1e-30, 3.0e38):
+        bc = fga.MaskBuilderConfig("avg_query_threshold", tau=tau)
+        m = fga.build_mask_avg_query(q, k, cfg, bc, device_result=True)
+        counts = m.counts.cpu().numpy().reshape(-1)
+        idx = m.idx.cpu().numpy().reshape(counts.size, -1)
+        for r in range(counts.size):
+            assert np.array_equal(idx[r, :counts[r]], _ref_threshold(rows[r], np.float32(tau))), (gain, tau, r)
