@@ -13,7 +13,7 @@ if not cuda_ok():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2509_16518_b200 as fga  # noqa: E402
-from paper_2509_16518_b200 import shard  # noqa: E402
+from paper_2509_16518_b200 import _lib, shard  # noqa: E402
 
 ATOL = 2e-2
 ATTN = [c for c in GOLDEN_CASES if c != "avgq_topk_ties"]
@@ -333,3 +333,47 @@ def test_sparse_attention_replays_in_a_cuda_graph():
     graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, fga.sparse_attention(q, k, v, mask, cfg))
+
+
+@pytest.mark.parametrize("strategy", ["avg_query_threshold", "avg_query_topk", "cached"])
+def test_mask_builders_replay_in_a_cuda_graph(strategy):
+    # one fga_build_mask_avgq / _cached call (pooled mean, score pass, compaction / selection and, for the
+    # threshold, the argmax fix-up) with caller-owned buffers: stream-ordered and allocation-free,
+    # so it captures into a CUDA graph and replays bitwise the eager lists
+    cfg = fga.AttnConfig(1, 2, 3000, 128, precision="bf16")
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k = (torch.randn(cfg.dims, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2))
+    shp = _lib.shape(*cfg.dims, cfg.group_size, cfg.scale)
+    rows, n = cfg.heads * cfg.num_groups, cfg.seq_len
+    op = _lib.FGA_WS_BUILD_CACHED if strategy == "cached" else _lib.FGA_WS_BUILD_AVGQ
+    ws = torch.empty(_lib.workspace_bytes(op, shp, 1), dtype=torch.uint8, device="cuda")
+    mode = _lib.FGA_SELECT_THRESHOLD if strategy.endswith("threshold") else _lib.FGA_SELECT_TOPK
+    tau = 1.7 / cfg.head_dim  # some groups keep nothing: the fix-up runs
+
+    def build(idx, cnt, st):
+        if strategy == "cached":
+            _lib.call("fga_build_mask_cached", q.data_ptr(), k.data_ptr(), shp, 0.02, 1, idx.data_ptr(), n,
+                      cnt.data_ptr(), 1, ws.data_ptr(), ws.numel(), st)
+            return
+        _lib.call("fga_build_mask_avgq", q.data_ptr(), k.data_ptr(), shp, mode, tau, 777, 1, idx.data_ptr(), n,
+                  cnt.data_ptr(), 1, ws.data_ptr(), ws.numel(), st)
+
+    idx_e = torch.empty((rows, n), dtype=torch.int32, device="cuda")
+    cnt_e = torch.empty(rows, dtype=torch.int32, device="cuda")
+    build(idx_e, cnt_e, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    idx = torch.full((rows, n), 5, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(rows, dtype=torch.int32, device="cuda")
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # (warm-up on a side stream, as torch.cuda.graph expects)
+        build(idx, cnt, side.cuda_stream)
+    torch.cuda.current_stream().wait_stream(side)
+    with torch.cuda.graph(graph):
+        build(idx, cnt, torch.cuda.current_stream().cuda_stream)
+    idx.fill_(5)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(cnt, cnt_e)
+    assert torch.equal(idx, idx_e)
