@@ -52,6 +52,9 @@ constexpr int STEP = 1024;  // keys per warp step
 #ifndef FGA_CK_BULK
 #define FGA_CK_BULK 1  // stage absolute int32 keys and write each step's aligned body with one TMA bulk store
 #endif
+#ifndef FGA_CK_EMIT
+#define FGA_CK_EMIT 1  // stage emission through a shared-memory address register (predicated STS + add per key)
+#endif
 constexpr int WARPS = FGA_CK_WARPS;
 constexpr int SPW = FGA_CK_SPW;    // steps per warp per round: 8 x 4 steps = 32768 keys (c2's whole row)
 constexpr int BUFS = FGA_CK_BUFS;  // stage buffers per warp (1: an extra __syncwarp per step)
@@ -73,10 +76,40 @@ __device__ __forceinline__ void emit16(uint16_t* st, int off, uint32_t m, int re
 }
 
 // the same for an int32 stage of absolute keys v0 + e
+#if !FGA_CK_EMIT
 __device__ __forceinline__ void emit16_i32(int32_t* st, int off, uint32_t m, int v0) {
 #pragma unroll
   for (int e = 0; e < 16; ++e)
     if (m & (1u << e)) st[off++] = v0 + e;
+}
+#endif
+
+// The same with the stage address carried in a register: per key slot one predicate test, the value,
+// a predicated STS and a predicated add (the C loop above compiles to ~6 instructions per slot, the
+// offset re-scaled into an address every time).  Returns the address past the last key written.
+#define FGA_EMIT1(M)                                  \
+  "and.b32 t, %2, " #M ";\n\t"                       \
+  "setp.ne.b32 p, t, 0;\n\t"                         \
+  "@p st.shared.b32 [%0], v;\n\t"                   \
+  "@p add.u32 %0, %0, 4;\n\t"                        \
+  "add.u32 v, v, 1;\n\t"
+#define FGA_EMIT8(A, B, C, D, E, F, G, H) \
+  FGA_EMIT1(A) FGA_EMIT1(B) FGA_EMIT1(C) FGA_EMIT1(D) FGA_EMIT1(E) FGA_EMIT1(F) FGA_EMIT1(G) FGA_EMIT1(H)
+#define FGA_EMIT_LO16 FGA_EMIT8(0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40, 0x80) \
+  FGA_EMIT8(0x100, 0x200, 0x400, 0x800, 0x1000, 0x2000, 0x4000, 0x8000)
+#define FGA_EMIT_HI16 FGA_EMIT8(0x10000, 0x20000, 0x40000, 0x80000, 0x100000, 0x200000, 0x400000, 0x800000) \
+  FGA_EMIT8(0x1000000, 0x2000000, 0x4000000, 0x8000000, 0x10000000, 0x20000000, 0x40000000, 0x80000000)
+
+template <int NB>
+__device__ __forceinline__ uint32_t emit_addr(uint32_t a, uint32_t m, int v0) {
+  static_assert(NB == 16 || NB == 32, "16 or 32 key slots");
+  if constexpr (NB == 16)
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t, v;\n\tmov.b32 v, %1;\n\t" FGA_EMIT_LO16 "}"
+                 : "+r"(a) : "r"(v0), "r"(m) : "memory");
+  else
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t, v;\n\tmov.b32 v, %1;\n\t" FGA_EMIT_LO16 FGA_EMIT_HI16 "}"
+                 : "+r"(a) : "r"(v0), "r"(m) : "memory");
+  return a;
 }
 
 __device__ __forceinline__ int warp_incl_scan(int v, int lane) {
@@ -206,8 +239,18 @@ __device__ __forceinline__ int compact_row(const Src& src, int64_t nsteps, int32
         if (lane == 0 && pending) bulk_wait_read_all();  // the previous step's bulk store has read the stage
         __syncwarp();
         const int shift = base & 3, tj = tot[j];
+#if FGA_CK_EMIT
+        if constexpr (!Src::kHalfMajor) {  // lane-major: the lane's 32 keys in one run
+          emit_addr<32>(static_cast<uint32_t>(__cvta_generic_to_shared(st + shift + o0[j])), m0[j] | (m1[j] << 16),
+                        kb + rel0);
+        } else {
+          emit_addr<16>(static_cast<uint32_t>(__cvta_generic_to_shared(st + shift + o0[j])), m0[j], kb + rel0);
+          emit_addr<16>(static_cast<uint32_t>(__cvta_generic_to_shared(st + shift + o1[j])), m1[j], kb + rel1);
+        }
+#else
         emit16_i32(st + shift, o0[j], m0[j], kb + rel0);
         emit16_i32(st + shift, o1[j], m1[j], kb + rel1);
+#endif
         if (bulk) fence_proxy_async_smem();  // the stage's generic-proxy writes -> the bulk store
         __syncwarp();
         const int i0 = bulk ? min(tj, (4 - shift) & 3) : tj;  // aligned body [i0, i1)
