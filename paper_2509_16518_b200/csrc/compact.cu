@@ -46,11 +46,17 @@ constexpr int STEP = 1024;  // keys per warp step
 #ifndef FGA_CK_MINB
 #define FGA_CK_MINB 5  // min CTAs per SM for __launch_bounds__ (caps registers at 48)
 #endif
+#ifndef FGA_CK_MINB_BYTES
+#define FGA_CK_MINB_BYTES FGA_CK_MINB  // the same for the keep-byte kernel
+#endif
 #ifndef FGA_CK_BUFS
 #define FGA_CK_BUFS 1
 #endif
 #ifndef FGA_CK_BULK
 #define FGA_CK_BULK 1  // stage absolute int32 keys and write each step's aligned body with one TMA bulk store
+#endif
+#ifndef FGA_CK_PERSIST
+#define FGA_CK_PERSIST 1  // bits: persistent CTAs (FGA_CK_MINB per SM) that prefetch the next row's words
 #endif
 #ifndef FGA_CK_EMIT
 #define FGA_CK_EMIT 1  // stage emission through a shared-memory address register (predicated STS + add per key)
@@ -187,18 +193,27 @@ struct BitSrc {
 constexpr int STAGE_N = FGA_CK_BULK ? STEP + 4 : STEP;
 using StageT = typename std::conditional<FGA_CK_BULK, int32_t, uint16_t>::type;
 
-template <class Src>
+// Optional cross-row prefetch (persistent bit compaction): `pref` holds the first round's data of
+// this row when `have_pref`, and receives the first round of `next` (if non-null) as soon as the last
+// round's scan is done, so those loads are in flight while this row is emitted.  `pending` (lane 0: a
+// bulk store may still be reading this warp's stage) carries across rows.
+template <class Src, class D = decltype(Src{}.load(0))>
 __device__ __forceinline__ int compact_row(const Src& src, int64_t nsteps, int32_t* __restrict__ out,
-                                           int (*s_warp)[WARPS], StageT (*stage)[STAGE_N]) {
+                                           int (*s_warp)[WARPS], StageT (*stage)[STAGE_N], bool& pending, int& rb,
+                                           D* pref = nullptr, bool have_pref = false, const Src* next = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int running = 0, rb = 0;
+  int running = 0;
   const bool bulk = FGA_CK_BULK && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
-  bool pending = false;  // lane 0: a bulk store may still be reading this warp's stage
   for (int64_t r0 = 0; r0 < nsteps; r0 += WARPS * SPW, rb ^= 1) {
     const int64_t s0 = r0 + int64_t(warp) * SPW;
-    decltype(src.load(0)) d[SPW];
+    D d[SPW];
+    if (pref != nullptr && have_pref && r0 == 0) {
 #pragma unroll
-    for (int j = 0; j < SPW; ++j) d[j] = src.load(s0 + j);  // all loads in flight first
+      for (int j = 0; j < SPW; ++j) d[j] = pref[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < SPW; ++j) d[j] = src.load(s0 + j);  // all loads in flight first
+    }
     uint32_t m0[SPW], m1[SPW];
     int o0[SPW], o1[SPW], tot[SPW], wsum = 0;
 #pragma unroll
@@ -219,6 +234,10 @@ __device__ __forceinline__ int compact_row(const Src& src, int64_t nsteps, int32
         tot[j] = t;
       }
       wsum += tot[j];
+    }
+    if (next != nullptr && r0 + WARPS * SPW >= nsteps) {
+#pragma unroll
+      for (int j = 0; j < SPW; ++j) pref[j] = next->load(int64_t(warp) * SPW + j);
     }
     if (lane == 0) s_warp[rb][warp] = wsum;
     __syncthreads();
@@ -277,11 +296,10 @@ __device__ __forceinline__ int compact_row(const Src& src, int64_t nsteps, int32
     }
     running += rtotal;
   }
-  if (FGA_CK_BULK && lane == 0 && pending) bulk_wait_all();  // stores complete before the CTA exits
   return running;
 }
 
-__global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_kernel(const uint8_t* __restrict__ keep,
+__global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB_BYTES) fga_compact_kernel(const uint8_t* __restrict__ keep,
                                                                 const float* __restrict__ scores, int64_t n,
                                                                 int32_t* __restrict__ idx, int64_t stride,
                                                                 int32_t* __restrict__ counts, int fill) {
@@ -295,7 +313,10 @@ __global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_kernel(co
   int32_t* out = idx + row * stride;
   const int head = static_cast<int>(reinterpret_cast<uintptr_t>(kr) & 15u);
   const ByteSrc src{kr - head, head, head + static_cast<int>(n), lane};
-  int running = compact_row(src, (head + n + STEP - 1) / STEP, out, s_warp, s_stage);
+  bool pending = false;
+  int rb = 0;
+  int running = compact_row(src, (head + n + STEP - 1) / STEP, out, s_warp, s_stage, pending, rb);
+  if (FGA_CK_BULK && lane == 0 && pending) bulk_wait_all();  // stores complete before the CTA exits
 
   if (running == 0 && scores != nullptr) {
     // argmax fallback, first maximum (np.argmax semantics)
@@ -344,25 +365,34 @@ __global__ void __launch_bounds__(256) fga_pack_bits_kernel(const uint8_t* __res
   }
 }
 
-__global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_bits_kernel(const uint32_t* __restrict__ bits, int64_t words,
+__global__ void __launch_bounds__(WARPS * 32, FGA_CK_MINB) fga_compact_bits_kernel(const uint32_t* __restrict__ bits, int64_t rows, int64_t words,
                                                                      int64_t n, int32_t* __restrict__ idx,
                                                                      int64_t stride, int32_t* __restrict__ counts,
                                                                      int fill, int32_t* __restrict__ fix_rows,
                                                                      int32_t* __restrict__ fix_count) {
   __shared__ int s_warp[2][WARPS];
   __shared__ __align__(16) StageT s_stage[WARPS * BUFS][STAGE_N];
-  const int64_t row = blockIdx.x;
   const int tid = threadIdx.x;
-  int32_t* out = idx + row * stride;
-  const BitSrc src{bits + row * words, words, n, tid & 31};
-  int running = compact_row(src, (words + 31) / 32, out, s_warp, s_stage);
-  if (running == 0 && fix_rows != nullptr) {  // argmax fallback of a fused threshold pass (masks.py:86-87):
-    if (tid == 0) fix_rows[atomicAdd(fix_count, 1)] = static_cast<int32_t>(row);  // out[0] by the fix-up
-    running = 1;
+  const int64_t nsteps = (words + 31) / 32;
+  bool pending = false;
+  int rb = 0;
+  uint32_t pref[SPW];
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    int32_t* out = idx + row * stride;
+    const BitSrc src{bits + row * words, words, n, tid & 31};
+    const int64_t nrow = row + gridDim.x;
+    const BitSrc nsrc{bits + (nrow < rows ? nrow : row) * words, words, n, tid & 31};
+    int running = compact_row(src, nsteps, out, s_warp, s_stage, pending, rb, pref, row != blockIdx.x,
+                              nrow < rows ? &nsrc : nullptr);
+    if (running == 0 && fix_rows != nullptr) {  // argmax fallback of a fused threshold pass (masks.py:86-87):
+      if (tid == 0) fix_rows[atomicAdd(fix_count, 1)] = static_cast<int32_t>(row);  // out[0] by the fix-up
+      running = 1;
+    }
+    if (tid == 0) counts[row] = running;
+    if (fill)
+      for (int64_t i = running + tid; i < n; i += WARPS * 32) out[i] = -1;
   }
-  if (tid == 0) counts[row] = running;
-  if (fill)
-    for (int64_t i = running + tid; i < n; i += WARPS * 32) out[i] = -1;
+  if (FGA_CK_BULK && (tid & 31) == 0 && pending) bulk_wait_all();  // stores complete before the CTA exits
 }
 
 }  // namespace
@@ -383,8 +413,11 @@ int launch_compact_bits(const uint32_t* bits, int64_t rows, int64_t n, int32_t* 
   if (n >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact_bits: n must be < 2^31");
   if (rows == 0) return FGA_OK;
   if (rows >= (int64_t(1) << 31)) return fail(FGA_EINVAL, "compact_bits: too many rows");
-  fga_compact_bits_kernel<<<static_cast<unsigned>(rows), WARPS * 32, 0, stream>>>(bits, (n + 31) / 32, n, idx, idx_stride,
-                                                                           counts, fill, fix_rows, fix_count);
+  const int64_t resident = int64_t(FGA_CK_MINB) * sm_count();
+  const int64_t grid = FGA_CK_PERSIST && rows > resident ? resident : rows;
+  fga_compact_bits_kernel<<<static_cast<unsigned>(grid), WARPS * 32, 0, stream>>>(bits, rows, (n + 31) / 32, n, idx,
+                                                                                idx_stride, counts, fill, fix_rows,
+                                                                                fix_count);
   return check_launch("fga_compact_bits_kernel");
 }
 

@@ -1,7 +1,12 @@
 """A/B of K1b compaction (fga_compact from keep bytes, fga_compact_bits from packed bits) across
 library builds at c2 (3072 rows x 32760 keys, ~45 % kept); outputs must agree bitwise.
 
-    python scripts/ab_compact.py lib1.so lib2.so ... [--dens 0.45]"""
+    python scripts/ab_compact.py lib1.so lib2.so ... [--dens 0.45] [--flush write|read]
+
+--batch B times B back-to-back launches per event pair (no flush in between; the 181 MB of lists
+exceed L2) -- the event clock ticks in ~2 us steps, too coarse for one 40 us launch.
+--flush read evicts L2 by reading a 512 MiB buffer after writing it, so the timed kernel does not
+start behind ~126 MB of dirty L2 lines from the flush (the default write flush leaves them)."""
 import ctypes
 import sys
 
@@ -20,6 +25,15 @@ keep = (torch.rand((rows, n), device="cuda", generator=gen) < dens).to(torch.uin
 bits = fga.pack_keep_bits(keep.view(1, 12, 256, n)).view(rows, -1).contiguous()
 st = torch.cuda.current_stream().cuda_stream
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+batch = int(sys.argv[sys.argv.index("--batch") + 1]) if "--batch" in sys.argv else 1
+fmode = sys.argv[sys.argv.index("--flush") + 1] if "--flush" in sys.argv else "write"
+fsum = torch.empty(1, dtype=torch.int64, device="cuda")
+
+
+def do_flush():
+    flush.zero_()
+    if fmode == "read":
+        torch.sum(flush.view(torch.int64), dim=0, out=fsum)
 P, I64 = ctypes.c_void_p, ctypes.c_int64
 fns, ref = [], {}
 for path in libs:
@@ -41,13 +55,14 @@ for rnd in range(6):
         for _ in range(2):
             assert fn() == 0
         for _ in range(5):
-            flush.zero_()
+            do_flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            fn()
+            for _ in range(batch):
+                fn()
             b.record()
             torch.cuda.synchronize()
-            times.setdefault(key, []).append(a.elapsed_time(b))
+            times.setdefault(key, []).append(a.elapsed_time(b) / batch)
 for key, name, idx, cnt, fn in fns:
     valid = torch.arange(n, device="cuda")[None, :] < cnt[:, None]
     got = torch.where(valid, idx, torch.full_like(idx, -1))
