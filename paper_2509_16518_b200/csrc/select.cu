@@ -36,7 +36,13 @@ namespace {
 #ifndef FGA_SEL_INTERP
 #define FGA_SEL_INTERP 1  // top-k: interpolation steps between the bisection steps
 #endif
-constexpr int SEL_THREADS = 512;
+#ifndef FGA_SEL_MINB
+#define FGA_SEL_MINB 2  // CTAs per SM for __launch_bounds__ (3 caps registers at 40; a c2 row is 64 KB of SMEM)
+#endif
+#ifndef FGA_SEL_THREADS
+#define FGA_SEL_THREADS 512
+#endif
+constexpr int SEL_THREADS = FGA_SEL_THREADS;
 constexpr int SEL_WARPS = SEL_THREADS / 32;
 
 // bf16 bits -> order-preserving unsigned key (negative values reversed below the positives)
@@ -73,7 +79,7 @@ __device__ __forceinline__ int block_sum(int v, int* red, int& phase) {
 }
 
 template <bool TOPK>
-__global__ void __launch_bounds__(SEL_THREADS, 2)
+__global__ void __launch_bounds__(SEL_THREADS, FGA_SEL_MINB)
     select_compact_kernel(const uint16_t* __restrict__ scores, int64_t n64, float tau, int64_t top_k,
                           int32_t* __restrict__ idx, int64_t stride, int32_t* __restrict__ counts, int fill) {
   extern __shared__ __align__(16) uint16_t s_key[];  // the row's bf16 bits, padded with -NaN to a multiple of 256
