@@ -14,7 +14,7 @@
 // packed bf16x2 compare over LDS.128 and a block sum -- instead of histogram atomics, which the
 // clustered scores of the builders serialise on a few bins (maskbuild.cu topk_kernel).
 //
-// One 512-thread CTA per (b,h,g) row:
+// One 256-thread CTA per (b,h,g) row:
 //   1. load: global bf16 -> SMEM (+ min / max of the order-preserving 16-bit keys),
 //   2. top-k: thr = the largest value v with #{s >= v} >= k (interpolation steps alternating
 //      with bisection steps over [min, max] keys),
@@ -37,10 +37,10 @@ namespace {
 #define FGA_SEL_INTERP 1  // top-k: interpolation steps between the bisection steps
 #endif
 #ifndef FGA_SEL_MINB
-#define FGA_SEL_MINB 2  // CTAs per SM for __launch_bounds__ (3 caps registers at 40; a c2 row is 64 KB of SMEM)
+#define FGA_SEL_MINB 3  // CTAs per SM for __launch_bounds__ (a c2 row is 64 KB of SMEM: 3 rows per SM)
 #endif
 #ifndef FGA_SEL_THREADS
-#define FGA_SEL_THREADS 512
+#define FGA_SEL_THREADS 256  // c2 top-k 188 -> 141 us, threshold 106 -> 92 us against 512 (128: 154 / 105, 1024: 334 / 197)
 #endif
 constexpr int SEL_THREADS = FGA_SEL_THREADS;
 constexpr int SEL_WARPS = SEL_THREADS / 32;
