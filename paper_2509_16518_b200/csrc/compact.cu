@@ -47,7 +47,7 @@ constexpr int STEP = 1024;  // keys per warp step
 #define FGA_CK_MINB 5  // min CTAs per SM for __launch_bounds__ (caps registers at 48)
 #endif
 #ifndef FGA_CK_MINB_BYTES
-#define FGA_CK_MINB_BYTES FGA_CK_MINB  // the same for the keep-byte kernel
+#define FGA_CK_MINB_BYTES 4  // the keep-byte kernel: 4 CTAs per SM (64 registers) beat 5 / 6 (61.3 / 63.6 / 76.5 us back to back)
 #endif
 #ifndef FGA_CK_BUFS
 #define FGA_CK_BUFS 1
