@@ -8,7 +8,7 @@ sys.path.insert(0, ".")
 import paper_2509_16518_b200 as fga  # noqa: E402
 
 g = torch.Generator(device="cuda").manual_seed(0)
-for n, m in ((1000, 128), (40001, 10000), (70003, 20000)):
+for n, m in ((1000, 128), (40001, 10000), (70003, 20000), (3000, 2)):  # (3000, 2): 3000 rows, persistent bits CTAs loop
     gr = -(-n // m)
     keep = (torch.rand((1, 2, gr, n), device="cuda", generator=g) < 0.4).to(torch.uint8)
     keep[0, 0, 1] = 0
