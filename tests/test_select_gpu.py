@@ -173,11 +173,12 @@ def test_build_mask_cached_single_call_equals_composition():
 
 
 @pytest.mark.parametrize("n,d,m", [(1000, 128, 128), (200, 64, 128), (4100, 128, 128), (1, 64, 1), (17, 128, 4),
-                                   (40, 64, 40)])
+                                   (40, 64, 40), (3000, 64, 2)])
 def test_fused_threshold_builder_bits_and_fallback(n, d, m):
     # threshold decided in the pooled-score epilogue (keep bits + argmax fix-up, fga_build_mask_avgq):
     # bit-exact with the reference selection on the same (bf16) scores, ragged N, 30% of the groups
-    # empty -> argmax fallback (masks.py:86-87); tiny N: the workspace covers the fused path
+    # empty -> argmax fallback (masks.py:86-87); tiny N: the workspace covers the fused path;
+    # (3000, 64, 2): 4500 rows, so the persistent bit-compaction CTAs loop over rows with fix-ups
     cfg = fga.AttnConfig(1, 3, n, d, group_size=m, precision="bf16")
     g = torch.Generator(device="cuda").manual_seed(n + d)
     q, k = (torch.randn(cfg.dims, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2))
