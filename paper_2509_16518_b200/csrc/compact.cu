@@ -7,7 +7,8 @@
 // Two input formats: uint8 keep bytes (fga_compact) and bit-packed keep words
 // (fga_compact_bits, 8x fewer bytes to read or to ship from the host).
 //
-// One 256-thread CTA per (b,h,g) row, walked in rounds of 8 warps x SPW steps
+// One 256-thread CTA per (b,h,g) row (keep bytes), or persistent CTAs looping over the rows
+// with the next row's words prefetched (keep bits, FGA_CK_PERSIST); a row is walked in rounds of 8 warps x SPW steps
 // of 1024 keys: warp w owns the contiguous steps [SPW*w, SPW*w + SPW) of the
 // round, so every lane issues all SPW steps' loads before it needs any of
 // them (keep bytes: lane l loads the 16-byte blocks at 16l and 512 + 16l of a
